@@ -1,0 +1,103 @@
+// boris_internal.h -- host-side declarations shared by libboris's translation units.
+// Not part of the ABI (include/libboris.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "boris_device.cuh"
+#include "libboris.h"
+
+namespace boris {
+
+constexpr int kStreamThreads = 256;  // SoA streaming kernel block size
+constexpr int kAosThreads = 256;     // AoS tile kernel block size (one particle / thread / tile)
+constexpr int kFusedThreads = 128;   // register-fused multi-step kernel block size
+constexpr int kFinalizeThreads = 1024;
+
+enum FieldKind { FK_ARRAYS = 0, FK_UNIFORM = 1, FK_PLANE_WAVE = 2, FK_MDIPOLE = 3 };
+
+struct SoaPtrs {
+    void *x, *y, *z, *px, *py, *pz, *w, *g;
+    int16_t *type;
+};
+
+struct FieldSoaPtrs {
+    const void *Ex, *Ey, *Ez, *Bx, *By, *Bz;
+};
+
+// Analytic field parameters prepared on the host for one push (FP = kernel
+// precision; phases in double, reading c5: t_n = t0 + n dt, never accumulated).
+template <typename FP>
+struct AnalyticArgs {
+    // uniform
+    FP E[3], B[3];
+    // plane wave: phi_n = (kvec . r) + ph0 - n * wdt ; E = cE cos(phi), B = cB cos(phi)
+    double kvec[3];  // k * k_hat
+    double ph0;      // phase0 - omega * t0
+    double wdt;      // omega * dt
+    FP cE[3];        // E0 * e_hat
+    FP cB[3];        // E0 * (k_hat x e_hat)
+    // m-dipole (eq. 14-15, readings c9-c13): time phase w0 t_n = w0t0 + n * w0dt
+    FP A0, k, k2;
+    double w0t0, w0dt;
+};
+
+// Per-launch description of an ensemble's storage.
+struct EnsView {
+    int precision;  // BORIS_FP32 / BORIS_FP64
+    int layout;     // BORIS_LAYOUT_*
+    int64_t n;
+    SoaPtrs soa;    // SoA
+    void *aos;      // AoS records
+};
+
+// Diagnostic partials: launchers report how many (ke, count) pairs they wrote.
+struct DiagOut {
+    double *partials;    // device scratch, capacity 2 * cap doubles
+    int64_t cap;         // pairs available
+    int64_t written;     // pairs written by the launch (0 if no diag)
+};
+
+int sm_count(int device);
+
+// Grid of a grid-stride launch: min(work blocks, SMs x resident blocks x waves).
+int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device);
+
+template <typename FP>
+cudaError_t launch_stream_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
+                              bool multi, DiagOut *diag, int device, cudaStream_t st);
+
+template <typename FP>
+cudaError_t launch_stream_aos(const EnsView &e, const void *field_records, const Coefs<FP> &co,
+                              bool multi, DiagOut *diag, int device, cudaStream_t st);
+
+template <typename FP>
+cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
+                         const Coefs<FP> &co, int64_t n_steps, bool multi, DiagOut *diag,
+                         int device, cudaStream_t st);
+
+template <typename FP>
+cudaError_t launch_kinetic_energy(const EnsView &e, const Coefs<FP> &co, bool multi,
+                                  DiagOut *diag, int device, cudaStream_t st);
+
+// Sum `pairs` (ke, count) partials in a fixed order into out[0..1].
+cudaError_t launch_diag_finalize(const double *partials, int64_t pairs, double *out,
+                                 cudaStream_t st);
+
+// Canonical double <-> layout conversion for upload/download (staging on device).
+// Staging layout: pos[3c], mom[3c], weight[c], gamma[c] (doubles), type[c] (int16).
+cudaError_t launch_from_canonical(const EnsView &e, int64_t first, int64_t count,
+                                  const double *d_pos, const double *d_mom, const double *d_w,
+                                  const int16_t *d_type, const double *d_gamma,
+                                  const double *d_inv_mc2_by_type, int n_types, int has_w,
+                                  int has_type, cudaStream_t st);
+cudaError_t launch_to_canonical(const EnsView &e, int64_t first, int64_t count, double *d_pos,
+                                double *d_mom, double *d_w, double *d_gamma, int16_t *d_type,
+                                cudaStream_t st);
+// Count type indices outside [0, n_types) into *d_bad (device int64).
+cudaError_t launch_check_types(const int16_t *type, int64_t stride_bytes, int64_t n,
+                               int n_types, unsigned long long *d_bad, cudaStream_t st);
+cudaError_t launch_fill_defaults(const EnsView &e, cudaStream_t st);
+
+}  // namespace boris

@@ -1,0 +1,292 @@
+// k_fused.cu -- register-fused multi-step Boris push for analytic fields
+// ("Analytical fields"; north_star "an analytic-field
+// variant that fuses n_steps iterations in registers so HBM is touched once
+// per launch"; SURVEY §8(a) row a12, Appendix A "Fused analytic kernel").
+//
+// One thread owns one particle for the whole launch: it reads r, p (and type,
+// weight) once, runs n_steps Boris steps with the field evaluated at
+// (r^n, t_n = t0 + n dt) in registers (reading c5), and writes r, p, gamma once.
+// The kernel is ALU-bound (FP32 FMA pipe for fp32, FP64 pipe for fp64).
+// fp32 kernels keep r in fp64 registers across steps (3 DADD per step on the
+// otherwise idle FP64 pipe) and evaluate the plane-wave phase in fp64 with an
+// exact 2-pi range reduction before the fp32 cosine (SURVEY §8(c) "GPU<->oracle,
+// fp32": this quadruples the margin under the 1e-5 bar at C4).
+#include "boris_internal.h"
+
+namespace boris {
+
+namespace {
+
+// 2 pi split for Cody-Waite range reduction in double.
+constexpr double kTwoPiHi = 6.283185307179586;
+constexpr double kTwoPiLo = 2.4492935982947064e-16;
+constexpr double kInvTwoPi = 0.15915494309189535;
+
+// cos(phi) for |phi| large: reduce in double, evaluate in FP.
+__device__ __forceinline__ float cos_reduced(double phi, float) {
+    const double q = rint(phi * kInvTwoPi);
+    double r = fma(-q, kTwoPiHi, phi);
+    r = fma(-q, kTwoPiLo, r);
+    return cosf((float)r);
+}
+__device__ __forceinline__ double cos_reduced(double phi, double) { return cos(phi); }
+
+__device__ __forceinline__ void sincos_fp(double a, double *s, double *c) { sincos(a, s, c); }
+__device__ __forceinline__ void sincos_fp(double a, float *s, float *c) {
+    const double q = rint(a * kInvTwoPi);
+    double r = fma(-q, kTwoPiHi, a);
+    r = fma(-q, kTwoPiLo, r);
+    sincosf((float)r, s, c);
+}
+
+// m-dipole radial functions (eq. 15, readings c11, c13): g1 = f1/xi, g2 = f2/xi^2, f3.
+// Taylor coefficients generated at compile time from their defining series:
+//   j0 = sum (-1)^n xi^{2n}/(2n+1)!,  j1/xi = sum (-1)^n 2(n+1) xi^{2n}/(2n+3)!,
+//   g2 = sum_{n>=1} (-1)^n [6(n+1)/(2n+3)! - 1/(2n+1)!] xi^{2n-2}.
+struct MdSeries {
+    double j0[10], j1x[10], g2[10];
+};
+constexpr double fact(int k) { return k <= 1 ? 1.0 : k * fact(k - 1); }
+constexpr MdSeries make_md_series() {
+    MdSeries s{};
+    for (int n = 0; n < 10; ++n) {
+        const double sg = (n % 2 == 0) ? 1.0 : -1.0;
+        s.j0[n] = sg / fact(2 * n + 1);
+        s.j1x[n] = sg * 2.0 * (n + 1) / fact(2 * n + 3);
+        s.g2[n] = sg * (6.0 * (n + 1) / fact(2 * n + 3) - 1.0 / fact(2 * n + 1));  // used n >= 1
+    }
+    return s;
+}
+__constant__ MdSeries c_md = make_md_series();
+
+template <typename FP>
+struct MdBranch;
+template <>
+struct MdBranch<double> {  // reading c13: fp64 xi* = 1, 9 terms
+    static constexpr double xi_star = 1.0;
+    static constexpr int terms = 9;
+};
+template <>
+struct MdBranch<float> {  // reading c13: fp32 xi* = 1.5, 7 terms
+    static constexpr float xi_star = 1.5f;
+    static constexpr int terms = 7;
+};
+
+template <typename FP>
+__device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
+    if (xi < MdBranch<FP>::xi_star) {
+        const FP x2 = xi * xi;
+        constexpr int T = MdBranch<FP>::terms;
+        FP j0 = FP(c_md.j0[T - 1]), j1x = FP(c_md.j1x[T - 1]), s2 = FP(c_md.g2[T - 1]);
+#pragma unroll
+        for (int n = T - 2; n >= 0; --n) {
+            j0 = j0 * x2 + FP(c_md.j0[n]);
+            j1x = j1x * x2 + FP(c_md.j1x[n]);
+        }
+#pragma unroll
+        for (int n = T - 2; n >= 1; --n) s2 = s2 * x2 + FP(c_md.g2[n]);
+        g1 = j1x;
+        g2 = s2;
+        f3 = j0 - j1x;
+    } else {
+        FP sn, cs;
+        if constexpr (sizeof(FP) == 4) sincosf(xi, &sn, &cs);
+        else sincos(xi, &sn, &cs);
+        const FP ix = FP(1) / xi, ix2 = ix * ix, ix3 = ix2 * ix;
+        const FP f1 = sn * ix2 - cs * ix;
+        const FP f2 = (FP(3) * ix3 - ix) * sn - FP(3) * cs * ix2;
+        f3 = (ix - ix3) * sn + cs * ix2;
+        g1 = f1 * ix;
+        g2 = f2 * ix2;
+    }
+}
+
+template <typename FP, int FIELD>
+__device__ __forceinline__ void analytic_field(const AnalyticArgs<FP> &fa, double rx, double ry,
+                                               double rz, int64_t n, FP &Ex, FP &Ey, FP &Ez,
+                                               FP &Bx, FP &By, FP &Bz) {
+    if constexpr (FIELD == FK_UNIFORM) {
+        Ex = fa.E[0]; Ey = fa.E[1]; Ez = fa.E[2];
+        Bx = fa.B[0]; By = fa.B[1]; Bz = fa.B[2];
+    } else if constexpr (FIELD == FK_PLANE_WAVE) {
+        // phi = k (k_hat . r) - omega t_n + phase0, t_n = t0 + n dt (reading c5)
+        const double phi = fma(fa.kvec[0], rx, fma(fa.kvec[1], ry, fa.kvec[2] * rz)) +
+                           (fa.ph0 - (double)n * fa.wdt);
+        const FP c = cos_reduced(phi, FP(0));
+        Ex = fa.cE[0] * c; Ey = fa.cE[1] * c; Ez = fa.cE[2] * c;
+        Bx = fa.cB[0] * c; By = fa.cB[1] * c; Bz = fa.cB[2] * c;
+    } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
+        const FP x = (FP)rx, y = (FP)ry, z = (FP)rz;
+        const FP R = sqrt(x * x + y * y + z * z);
+        FP g1, g2, f3;
+        md_radial<FP>(fa.k * R, g1, g2, f3);
+        FP swt, cwt;
+        sincos_fp(fa.w0t0 + (double)n * fa.w0dt, &swt, &cwt);
+        const FP ce = FP(2) * fa.A0 * cwt * fa.k * g1;  // 2 A0 cos(w t) f1/R
+        const FP sb = FP(-2) * fa.A0 * swt;              // -2 A0 sin(w t)
+        const FP k2g2 = fa.k2 * g2;                      // f2/R^2
+        Ex = -ce * y;
+        Ey = ce * x;
+        Ez = FP(0);
+        Bx = sb * k2g2 * x * z;
+        By = sb * k2g2 * y * z;
+        Bz = sb * (k2g2 * z * z + f3);
+    }
+}
+
+// Position accumulator: double for fp32 state (see header), FP otherwise.
+template <typename FP, int LAYOUT>
+struct Particle {
+    static __device__ __forceinline__ void load(const EnsView &e, int64_t i, double &x, double &y,
+                                                double &z, FP &px, FP &py, FP &pz, FP &w,
+                                                int &ty) {
+        if constexpr (LAYOUT == BORIS_LAYOUT_SOA) {
+            x = ((const FP *)e.soa.x)[i];
+            y = ((const FP *)e.soa.y)[i];
+            z = ((const FP *)e.soa.z)[i];
+            px = ((const FP *)e.soa.px)[i];
+            py = ((const FP *)e.soa.py)[i];
+            pz = ((const FP *)e.soa.pz)[i];
+            w = e.soa.w ? ((const FP *)e.soa.w)[i] : FP(1);
+            ty = e.soa.type ? e.soa.type[i] : 0;
+        } else {
+            constexpr int RB = sizeof(FP) == 4 ? 36 : 72;
+            const unsigned char *rec = (const unsigned char *)e.aos + i * RB;
+            const FP *r = (const FP *)rec;
+            x = r[0]; y = r[1]; z = r[2];
+            px = r[3]; py = r[4]; pz = r[5];
+            w = r[6];
+            ty = *(const int16_t *)(rec + 8 * sizeof(FP));
+        }
+    }
+    static __device__ __forceinline__ void store(const EnsView &e, int64_t i, double x, double y,
+                                                 double z, FP px, FP py, FP pz, FP g) {
+        if constexpr (LAYOUT == BORIS_LAYOUT_SOA) {
+            ((FP *)e.soa.x)[i] = (FP)x;
+            ((FP *)e.soa.y)[i] = (FP)y;
+            ((FP *)e.soa.z)[i] = (FP)z;
+            ((FP *)e.soa.px)[i] = px;
+            ((FP *)e.soa.py)[i] = py;
+            ((FP *)e.soa.pz)[i] = pz;
+            ((FP *)e.soa.g)[i] = g;
+        } else {
+            constexpr int RB = sizeof(FP) == 4 ? 36 : 72;
+            FP *r = (FP *)((unsigned char *)e.aos + i * RB);
+            r[0] = (FP)x; r[1] = (FP)y; r[2] = (FP)z;
+            r[3] = px; r[4] = py; r[5] = pz;
+            r[7] = g;
+        }
+    }
+};
+
+}  // namespace
+
+template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG>
+__global__ void __launch_bounds__(kFusedThreads)
+    k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
+            const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
+    __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
+    if (MULTI) load_type_table(co, s_t, s_ke);
+    double ke = 0.0, cnt = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kFusedThreads;
+    for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride) {
+        double x, y, z;
+        FP px, py, pz, w;
+        int ty;
+        Particle<FP, LAYOUT>::load(e, i, x, y, z, px, py, pz, w, ty);
+        if (!MULTI) ty = 0;
+        const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
+        FP ux = px * tc.inv_mc, uy = py * tc.inv_mc, uz = pz * tc.inv_mc;
+        FP gam = FP(1);
+        for (int64_t s = 0; s < n_steps; ++s) {
+            FP Ex, Ey, Ez, Bx, By, Bz;
+            analytic_field<FP, FIELD>(fa, x, y, z, s, Ex, Ey, Ez, Bx, By, Bz);
+            const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc.alpha, gam);
+            const FP ct = co.cdt * inv_g;
+            // a10 (eq. 7) with the position accumulated in double
+            x += (double)(ct * ux);
+            y += (double)(ct * uy);
+            z += (double)(ct * uz);
+        }
+        if (n_steps == 0) gam = b_sqrt(FP(1) + (ux * ux + uy * uy + uz * uz));
+        Particle<FP, LAYOUT>::store(e, i, x, y, z, ux * tc.mc, uy * tc.mc, uz * tc.mc, gam);
+        if (DIAG) {
+            ke += kinetic_energy<FP>(ux, uy, uz, gam, w, MULTI ? s_ke[ty] : co.ke[0]);
+            cnt += 1.0;
+        }
+    }
+    if (DIAG) block_diag_partial<kFusedThreads>(ke, cnt, partials);
+}
+
+template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG>
+static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
+                                  const Coefs<FP> &co, int64_t n_steps, DiagOut *diag,
+                                  int device, cudaStream_t st) {
+    const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
+    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads, device);
+    if (DIAG && grid > diag->cap) grid = diag->cap;
+    k_fused<FP, LAYOUT, FIELD, MULTI, DIAG><<<(unsigned)grid, kFusedThreads, 0, st>>>(
+        e, fa, co, n_steps, diag ? diag->partials : nullptr);
+    if (diag) diag->written = DIAG ? grid : 0;
+    return cudaGetLastError();
+}
+
+template <typename FP, int LAYOUT, int FIELD>
+static cudaError_t dispatch_fused_md(const EnsView &e, const AnalyticArgs<FP> &fa,
+                                     const Coefs<FP> &co, int64_t n_steps, bool multi,
+                                     DiagOut *diag, int device, cudaStream_t st) {
+    if (multi)
+        return diag ? dispatch_fused<FP, LAYOUT, FIELD, true, true>(e, fa, co, n_steps, diag,
+                                                                     device, st)
+                    : dispatch_fused<FP, LAYOUT, FIELD, true, false>(e, fa, co, n_steps, diag,
+                                                                      device, st);
+    return diag ? dispatch_fused<FP, LAYOUT, FIELD, false, true>(e, fa, co, n_steps, diag,
+                                                                  device, st)
+                : dispatch_fused<FP, LAYOUT, FIELD, false, false>(e, fa, co, n_steps, diag,
+                                                                   device, st);
+}
+
+template <typename FP, int LAYOUT>
+static cudaError_t dispatch_fused_field(const EnsView &e, int field_kind,
+                                        const AnalyticArgs<FP> &fa, const Coefs<FP> &co,
+                                        int64_t n_steps, bool multi, DiagOut *diag, int device,
+                                        cudaStream_t st) {
+    switch (field_kind) {
+    case FK_UNIFORM:
+        return dispatch_fused_md<FP, LAYOUT, FK_UNIFORM>(e, fa, co, n_steps, multi, diag, device,
+                                                         st);
+    case FK_PLANE_WAVE:
+        return dispatch_fused_md<FP, LAYOUT, FK_PLANE_WAVE>(e, fa, co, n_steps, multi, diag,
+                                                            device, st);
+    case FK_MDIPOLE:
+        return dispatch_fused_md<FP, LAYOUT, FK_MDIPOLE>(e, fa, co, n_steps, multi, diag, device,
+                                                         st);
+    default:
+        return cudaErrorInvalidValue;
+    }
+}
+
+template <typename FP>
+cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
+                         const Coefs<FP> &co, int64_t n_steps, bool multi, DiagOut *diag,
+                         int device, cudaStream_t st) {
+    if (e.n == 0) {
+        if (diag) diag->written = 0;
+        return cudaSuccess;
+    }
+    if (e.layout == BORIS_LAYOUT_SOA)
+        return dispatch_fused_field<FP, BORIS_LAYOUT_SOA>(e, field_kind, fa, co, n_steps, multi,
+                                                          diag, device, st);
+    return dispatch_fused_field<FP, BORIS_LAYOUT_AOS>(e, field_kind, fa, co, n_steps, multi,
+                                                      diag, device, st);
+}
+
+template cudaError_t launch_fused<float>(const EnsView &, int, const AnalyticArgs<float> &,
+                                         const Coefs<float> &, int64_t, bool, DiagOut *, int,
+                                         cudaStream_t);
+template cudaError_t launch_fused<double>(const EnsView &, int, const AnalyticArgs<double> &,
+                                          const Coefs<double> &, int64_t, bool, DiagOut *, int,
+                                          cudaStream_t);
+
+}  // namespace boris

@@ -1,0 +1,232 @@
+// k_stream_aos.cu -- single-step AoS Boris push with TMA bulk-copy tile staging
+// (paper §3 "Particle" records; AoS vs SoA L237-250;
+// SURVEY §8(a) rows a1-a13, Appendix A "AoS kernel").
+//
+// Records are 36 B (fp32) / 72 B (fp64): per-thread global loads would be
+// stride-36/72 and uncoalesced.  Instead each CTA is a persistent pipeline:
+// one elected thread streams tiles of kAosThreads records (+ their {E,B} field
+// records) HBM -> shared memory with 1-D TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx), STAGES tiles in flight; every
+// thread pushes one particle in shared memory (record stride 9 words fp32 /
+// 18 words fp64: bank-conflict free), then the elected thread writes the whole
+// tile back with one bulk store (cp.async.bulk.global.shared::cta).  Writing
+// full records keeps every DRAM sector fully written (no read-modify-write).
+// Layout-implied traffic: fp32 36+24 read + 36 write = 96 B/particle-step.
+#include "boris_internal.h"
+
+namespace boris {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+// TMA 1-D bulk copy global -> shared, completion signalled on `bar` (tx bytes).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// TMA 1-D bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// Make generic-proxy shared-memory writes visible to the async (TMA) proxy.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <typename FP>
+struct AosGeom {
+    static constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32
+                                              : BORIS_AOS_RECORD_BYTES_FP64;
+    static constexpr int FB = 6 * (int)sizeof(FP);
+    static constexpr int TP = kAosThreads;           // particles per tile
+    static constexpr int STAGES = sizeof(FP) == 4 ? 4 : 3;
+    static constexpr int TILE_R = TP * RB;           // 9216 / 18432 B
+    static constexpr int TILE_F = TP * FB;           // 6144 / 12288 B
+    static constexpr int SMEM = STAGES * (TILE_R + TILE_F) + STAGES * 8;
+    static constexpr int TYPE_OFF = 8 * (int)sizeof(FP);  // 32 / 64
+    // bulk copies move multiples of 16 B: tiles cover a multiple of ALIGN particles
+    static constexpr int ALIGN = sizeof(FP) == 4 ? 4 : 2;
+};
+
+// Push particle j of a shared-memory record tile (record layout of libboris.h).
+template <typename FP, bool MULTI, bool DIAG>
+__device__ __forceinline__ void push_record(unsigned char *rec, const FP *fld,
+                                            const Coefs<FP> &co, const TypeCoef<FP> *s_t,
+                                            const double *s_ke, double &ke, double &cnt) {
+    FP *r = (FP *)rec;
+    const int ty = MULTI ? *(const int16_t *)(rec + AosGeom<FP>::TYPE_OFF) : 0;
+    const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
+    FP ux, uy, uz, gam;
+    push_one<FP>(r[0], r[1], r[2], r[3], r[4], r[5], gam, fld[0], fld[1], fld[2], fld[3], fld[4],
+                 fld[5], tc, co.cdt, ux, uy, uz);
+    r[7] = gam;
+    if (DIAG) {
+        ke += kinetic_energy<FP>(ux, uy, uz, gam, r[6], MULTI ? s_ke[ty] : co.ke[0]);
+        cnt += 1.0;
+    }
+}
+
+}  // namespace
+
+template <typename FP, bool MULTI, bool DIAG>
+__global__ void __launch_bounds__(kAosThreads)
+    k_stream_aos(unsigned char *rec, const unsigned char *frec,
+                 const __grid_constant__ Coefs<FP> co, int64_t n_tiles, int64_t n_main,
+                 int64_t n, double *partials) {
+    using Gm = AosGeom<FP>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char *s_rec = smem;
+    unsigned char *s_fld = smem + Gm::STAGES * Gm::TILE_R;
+    uint64_t *bar = (uint64_t *)(s_fld + Gm::STAGES * Gm::TILE_F);
+    __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Gm::STAGES; ++s) mbar_init(&bar[s], 1);
+        fence_proxy_async_smem();
+    }
+    if (MULTI) load_type_table(co, s_t, s_ke);  // contains __syncthreads
+    else __syncthreads();
+
+    auto tile_count = [&](int64_t t) -> int {
+        const int64_t c = n_main - t * Gm::TP;
+        return c < Gm::TP ? (int)c : Gm::TP;
+    };
+    auto issue = [&](int64_t t, int s) {
+        const int c = tile_count(t);
+        const uint32_t br = (uint32_t)c * Gm::RB, bf = (uint32_t)c * Gm::FB;
+        mbar_arrive_expect_tx(&bar[s], br + bf);
+        bulk_g2s(s_rec + s * Gm::TILE_R, rec + t * Gm::TILE_R, br, &bar[s]);
+        bulk_g2s(s_fld + s * Gm::TILE_F, frec + t * Gm::TILE_F, bf, &bar[s]);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Gm::STAGES; ++s) {
+            const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+            if (t < n_tiles) issue(t, s);
+        }
+    }
+
+    double ke = 0.0, cnt = 0.0;
+    for (int64_t k = 0;; ++k) {
+        const int64_t t = blockIdx.x + k * gridDim.x;
+        if (t >= n_tiles) break;
+        const int s = (int)(k % Gm::STAGES);
+        mbar_wait(&bar[s], (uint32_t)((k / Gm::STAGES) & 1));
+        const int c = tile_count(t);
+        if ((int)threadIdx.x < c)
+            push_record<FP, MULTI, DIAG>(s_rec + s * Gm::TILE_R + threadIdx.x * Gm::RB,
+                                         (const FP *)(s_fld + s * Gm::TILE_F) + threadIdx.x * 6,
+                                         co, s_t, s_ke, ke, cnt);
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_s2g(rec + t * Gm::TILE_R, s_rec + s * Gm::TILE_R, (uint32_t)c * Gm::RB);
+            bulk_commit();
+            const int64_t tn = t + (int64_t)Gm::STAGES * gridDim.x;
+            if (tn < n_tiles) {
+                bulk_wait_read_all();  // the stage's smem has been read out by the store
+                issue(tn, s);
+            }
+        }
+    }
+    // ragged tail (< ALIGN particles not covered by 16 B-multiple tiles): direct access
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - n_main) {
+        const int64_t i = n_main + threadIdx.x;
+        push_record<FP, MULTI, DIAG>(rec + i * Gm::RB, (const FP *)(frec + i * Gm::FB), co, s_t,
+                                     s_ke, ke, cnt);
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+    if (DIAG) block_diag_partial<kAosThreads>(ke, cnt, partials);
+}
+
+template <typename FP, bool MULTI, bool DIAG>
+static cudaError_t dispatch_aos(const EnsView &e, const void *frec, const Coefs<FP> &co,
+                                DiagOut *diag, int device, cudaStream_t st) {
+    using Gm = AosGeom<FP>;
+    auto kern = k_stream_aos<FP, MULTI, DIAG>;
+    static bool attr_set[64] = {};  // per device
+    if (device >= 0 && device < 64 && !attr_set[device]) {
+        cudaError_t err =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Gm::SMEM);
+        if (err != cudaSuccess) return err;
+        attr_set[device] = true;
+    }
+    int per_sm = 0;
+    cudaError_t err =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAosThreads, Gm::SMEM);
+    if (err != cudaSuccess) return err;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t n_main = e.n / Gm::ALIGN * Gm::ALIGN;
+    const int64_t n_tiles = (n_main + Gm::TP - 1) / Gm::TP;
+    int64_t grid = (int64_t)sm_count(device) * per_sm;
+    if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
+    if (DIAG && grid > diag->cap) grid = diag->cap;
+    kern<<<(unsigned)grid, kAosThreads, Gm::SMEM, st>>>(
+        (unsigned char *)e.aos, (const unsigned char *)frec, co, n_tiles, n_main, e.n,
+        diag ? diag->partials : nullptr);
+    if (diag) diag->written = DIAG ? grid : 0;
+    return cudaGetLastError();
+}
+
+template <typename FP>
+cudaError_t launch_stream_aos(const EnsView &e, const void *field_records, const Coefs<FP> &co,
+                              bool multi, DiagOut *diag, int device, cudaStream_t st) {
+    if (e.n == 0) {
+        if (diag) diag->written = 0;
+        return cudaSuccess;
+    }
+    const bool d = diag != nullptr;
+    if (multi)
+        return d ? dispatch_aos<FP, true, true>(e, field_records, co, diag, device, st)
+                 : dispatch_aos<FP, true, false>(e, field_records, co, diag, device, st);
+    return d ? dispatch_aos<FP, false, true>(e, field_records, co, diag, device, st)
+             : dispatch_aos<FP, false, false>(e, field_records, co, diag, device, st);
+}
+
+template cudaError_t launch_stream_aos<float>(const EnsView &, const void *,
+                                              const Coefs<float> &, bool, DiagOut *, int,
+                                              cudaStream_t);
+template cudaError_t launch_stream_aos<double>(const EnsView &, const void *,
+                                               const Coefs<double> &, bool, DiagOut *, int,
+                                               cudaStream_t);
+
+}  // namespace boris

@@ -1,0 +1,193 @@
+// k_stream_soa.cu -- single-step SoA streaming Boris push ("precalculated
+// fields").
+//
+// HBM-bound: per particle-step fp32 reads r,p,E,B (48 B) and writes r,p,gamma
+// (28 B) = 76 B (+4 B weight with the KE diagnostic, +2 B type if multi-type).
+// Design: one thread owns 16 B of every component array (4 fp32
+// or 2 fp64 particles), so each component moves with one 128-bit access per
+// thread and a warp touches 512 contiguous bytes per array; all loads of a
+// group are issued before any arithmetic (12 x LDG.128 in flight per thread).
+// Grid-stride over groups with a grid sized to the resident-block count.
+#include "boris_internal.h"
+
+namespace boris {
+
+template <typename FP, bool MULTI, bool DIAG>
+__global__ void __launch_bounds__(kStreamThreads)
+    k_stream_soa_vec(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ Coefs<FP> co,
+                     int64_t n_groups, int64_t n, double *partials) {
+    constexpr int V = Vec<FP>::N;
+    __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
+    if (MULTI) load_type_table(co, s_t, s_ke);
+
+    FP *__restrict__ X = (FP *)s.x;
+    FP *__restrict__ Y = (FP *)s.y;
+    FP *__restrict__ Z = (FP *)s.z;
+    FP *__restrict__ PX = (FP *)s.px;
+    FP *__restrict__ PY = (FP *)s.py;
+    FP *__restrict__ PZ = (FP *)s.pz;
+    FP *__restrict__ G = (FP *)s.g;
+    const FP *__restrict__ W = (const FP *)s.w;
+    const FP *__restrict__ EX = (const FP *)f.Ex;
+    const FP *__restrict__ EY = (const FP *)f.Ey;
+    const FP *__restrict__ EZ = (const FP *)f.Ez;
+    const FP *__restrict__ BX = (const FP *)f.Bx;
+    const FP *__restrict__ BY = (const FP *)f.By;
+    const FP *__restrict__ BZ = (const FP *)f.Bz;
+
+    double ke = 0.0, cnt = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
+    for (int64_t grp = (int64_t)blockIdx.x * kStreamThreads + threadIdx.x; grp < n_groups;
+         grp += stride) {
+        const int64_t i0 = grp * V;
+        Vec<FP> x, y, z, px, py, pz, ex, ey, ez, bx, by, bz, w, gm;
+        // a1/a2: issue every load of the group before any arithmetic
+        x.load_state(X + i0);
+        y.load_state(Y + i0);
+        z.load_state(Z + i0);
+        px.load_state(PX + i0);
+        py.load_state(PY + i0);
+        pz.load_state(PZ + i0);
+        ex.load_field(EX + i0);
+        ey.load_field(EY + i0);
+        ez.load_field(EZ + i0);
+        bx.load_field(BX + i0);
+        by.load_field(BY + i0);
+        bz.load_field(BZ + i0);
+        int ty[V];
+        if (MULTI) load_types<V>(s.type + i0, ty);
+        if (DIAG) {
+            if (W) w.load_field(W + i0);
+            else {
+#pragma unroll
+                for (int j = 0; j < V; ++j) w.v[j] = FP(1);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const TypeCoef<FP> tc = MULTI ? s_t[ty[j]] : co.t[0];
+            FP ux, uy, uz;
+            push_one<FP>(x.v[j], y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], gm.v[j], ex.v[j],
+                         ey.v[j], ez.v[j], bx.v[j], by.v[j], bz.v[j], tc, co.cdt, ux, uy, uz);
+            if (DIAG) {
+                ke += kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j],
+                                         MULTI ? s_ke[ty[j]] : co.ke[0]);
+                cnt += 1.0;
+            }
+        }
+        x.store(X + i0);
+        y.store(Y + i0);
+        z.store(Z + i0);
+        px.store(PX + i0);
+        py.store(PY + i0);
+        pz.store(PZ + i0);
+        gm.store(G + i0);
+    }
+    // ragged tail: the last n - V*n_groups (< V) particles, scalar loads, same arithmetic
+    const int64_t tail0 = n_groups * V;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail0) {
+        const int64_t i = tail0 + threadIdx.x;
+        const TypeCoef<FP> tc = MULTI ? s_t[s.type[i]] : co.t[0];
+        FP ux, uy, uz, gam;
+        FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
+        push_one<FP>(x, y, z, px, py, pz, gam, EX[i], EY[i], EZ[i], BX[i], BY[i], BZ[i], tc,
+                     co.cdt, ux, uy, uz);
+        X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
+        if (DIAG) {
+            ke += kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1),
+                                     MULTI ? s_ke[s.type[i]] : co.ke[0]);
+            cnt += 1.0;
+        }
+    }
+    if (DIAG) block_diag_partial<kStreamThreads>(ke, cnt, partials);
+}
+
+// Unaligned inputs (e.g. sliced torch tensors): one particle per thread, scalar
+// accesses, the same push_one arithmetic.
+template <typename FP, bool MULTI, bool DIAG>
+__global__ void __launch_bounds__(kStreamThreads)
+    k_stream_soa_scalar(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ Coefs<FP> co,
+                        int64_t n, double *partials) {
+    __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
+    if (MULTI) load_type_table(co, s_t, s_ke);
+    FP *X = (FP *)s.x, *Y = (FP *)s.y, *Z = (FP *)s.z;
+    FP *PX = (FP *)s.px, *PY = (FP *)s.py, *PZ = (FP *)s.pz, *G = (FP *)s.g;
+    const FP *W = (const FP *)s.w;
+    const FP *EX = (const FP *)f.Ex, *EY = (const FP *)f.Ey, *EZ = (const FP *)f.Ez;
+    const FP *BX = (const FP *)f.Bx, *BY = (const FP *)f.By, *BZ = (const FP *)f.Bz;
+    double ke = 0.0, cnt = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
+    for (int64_t i = (int64_t)blockIdx.x * kStreamThreads + threadIdx.x; i < n; i += stride) {
+        const int ty = MULTI ? s.type[i] : 0;
+        const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
+        FP ux, uy, uz, gam;
+        FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
+        push_one<FP>(x, y, z, px, py, pz, gam, EX[i], EY[i], EZ[i], BX[i], BY[i], BZ[i], tc,
+                     co.cdt, ux, uy, uz);
+        X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
+        if (DIAG) {
+            ke += kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1),
+                                     MULTI ? s_ke[ty] : co.ke[0]);
+            cnt += 1.0;
+        }
+    }
+    if (DIAG) block_diag_partial<kStreamThreads>(ke, cnt, partials);
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+template <typename FP, bool MULTI, bool DIAG>
+static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
+                                DiagOut *diag, int device, cudaStream_t st) {
+    constexpr int V = Vec<FP>::N;
+    const bool vec = aligned16(e.soa.x) && aligned16(e.soa.y) && aligned16(e.soa.z) &&
+                     aligned16(e.soa.px) && aligned16(e.soa.py) && aligned16(e.soa.pz) &&
+                     aligned16(e.soa.g) && aligned16(f.Ex) && aligned16(f.Ey) &&
+                     aligned16(f.Ez) && aligned16(f.Bx) && aligned16(f.By) && aligned16(f.Bz) &&
+                     (!DIAG || e.soa.w == nullptr || aligned16(e.soa.w)) &&
+                     (!MULTI || ((uintptr_t)e.soa.type & (2 * V - 1)) == 0);
+    double *partials = diag ? diag->partials : nullptr;
+    int64_t grid;
+    if (vec) {
+        const int64_t n_groups = e.n / V;
+        const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
+        grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+        if (DIAG && grid > diag->cap) grid = diag->cap;
+        k_stream_soa_vec<FP, MULTI, DIAG>
+            <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, co, n_groups, e.n, partials);
+    } else {
+        const int64_t blocks = (e.n + kStreamThreads - 1) / kStreamThreads;
+        grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+        if (DIAG && grid > diag->cap) grid = diag->cap;
+        k_stream_soa_scalar<FP, MULTI, DIAG>
+            <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, co, e.n, partials);
+    }
+    if (diag) diag->written = DIAG ? grid : 0;
+    return cudaGetLastError();
+}
+
+template <typename FP>
+cudaError_t launch_stream_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
+                              bool multi, DiagOut *diag, int device, cudaStream_t st) {
+    if (e.n == 0) {
+        if (diag) diag->written = 0;
+        return cudaSuccess;
+    }
+    const bool d = diag != nullptr;
+    if (multi)
+        return d ? dispatch_soa<FP, true, true>(e, f, co, diag, device, st)
+                 : dispatch_soa<FP, true, false>(e, f, co, diag, device, st);
+    return d ? dispatch_soa<FP, false, true>(e, f, co, diag, device, st)
+             : dispatch_soa<FP, false, false>(e, f, co, diag, device, st);
+}
+
+template cudaError_t launch_stream_soa<float>(const EnsView &, const FieldSoaPtrs &,
+                                              const Coefs<float> &, bool, DiagOut *, int,
+                                              cudaStream_t);
+template cudaError_t launch_stream_soa<double>(const EnsView &, const FieldSoaPtrs &,
+                                               const Coefs<double> &, bool, DiagOut *, int,
+                                               cudaStream_t);
+
+}  // namespace boris

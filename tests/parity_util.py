@@ -1,0 +1,87 @@
+"""Shared helpers for GPU <-> oracle parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle
+
+# Tolerances from BASELINE.json north_star: "relative error <= 1e-12 for fp64 and
+# <= 1e-5 for fp32 after 100 steps", with the metric of reading c15.
+TOL = {"fp64": 1e-12, "fp32": 1e-5}
+
+
+class C15:
+    """Reading c15: per particle ||x_gpu - x_ref|| / (||x_ref|| + S_x), with S_x the
+    trajectory scale max_{s' <= s} rms_j ||x_ref,j(s')||."""
+
+    def __init__(self):
+        self.scale = {"r": 0.0, "p": 0.0}
+
+    def __call__(self, key, gpu, ref):
+        nrm = np.linalg.norm(ref, axis=1)
+        if nrm.size:
+            self.scale[key] = max(self.scale[key], float(np.sqrt(np.mean(nrm ** 2))))
+        s = self.scale[key] if self.scale[key] > 0 else 1.0
+        err = np.linalg.norm(gpu - ref, axis=1) / (nrm + s)
+        return float(err.max()) if err.size else 0.0
+
+
+def rounded(d, precision):
+    """The generator's float64 values rounded to the kernel's storage precision (the
+    oracle starts from the same rounded inputs, reading c15)."""
+    dt = torch.float32 if precision == "fp32" else torch.float64
+    out = {}
+    for k, v in d.items():
+        out[k] = v.to(dt).to(torch.float64) if v.dtype == torch.float64 else v.clone()
+    return out
+
+
+def stack3(d, a, b, c):
+    return torch.stack([d[a], d[b], d[c]], 1).numpy().astype(np.float64)
+
+
+def oracle_field(w, precision, xi=None):
+    """Oracle (kind, params) for a synth.Workload's analytic field."""
+    if w.field_kind == "uniform":
+        return oracle.FIELD_UNIFORM, list(w.uniform_E) + list(w.uniform_B)
+    if w.field_kind == "plane_wave":
+        pw = w.plane_wave
+        return oracle.FIELD_PLANE_WAVE, ([pw["E0"]] + list(pw["k_hat"]) + list(pw["e_hat"]) +
+                                         [pw["omega"], pw["k"], pw["phase0"]])
+    if w.field_kind == "mdipole":
+        md = w.plane_wave  # reuse dict slot: A0, omega0, k
+        xs, nt = (1.0, 9) if precision == "fp64" else (1.5, 7)
+        return oracle.FIELD_MDIPOLE, [md["A0"], md["omega0"], md["k"], xs, nt]
+    return oracle.FIELD_ARRAYS, None
+
+
+class OracleRun:
+    """The oracle's state for one workload, advanced in chunks like the GPU."""
+
+    def __init__(self, w, d, precision):
+        self.w = w
+        self.pos = stack3(d, "x", "y", "z")
+        self.mom = stack3(d, "px", "py", "pz")
+        self.type = d["type"].numpy().astype(np.int16)
+        self.weight = d["weight"].numpy().astype(np.float64)
+        self.tq = [q for q, m in w.types]
+        self.tm = [m for q, m in w.types]
+        self.kind, self.params = oracle_field(w, precision)
+        if self.kind == oracle.FIELD_ARRAYS:
+            self.E = stack3(d, "Ex", "Ey", "Ez")
+            self.B = stack3(d, "Bx", "By", "Bz")
+        else:
+            self.E = self.B = None
+        self.t = 0.0
+        self.gamma = None
+
+    def push(self, n_steps):
+        self.pos, self.mom, self.gamma = oracle.push(
+            self.pos, self.mom, self.type, self.tq, self.tm, self.w.light_velocity, self.kind,
+            self.params, E=self.E, B=self.B, t0=self.t, dt=self.w.dt, n_steps=n_steps)
+        self.t += n_steps * self.w.dt
+
+    def kinetic_energy(self):
+        return oracle.kinetic_energy(self.mom, self.gamma, self.weight, self.type, self.tm,
+                                     self.w.light_velocity)

@@ -1,0 +1,432 @@
+"""GPU (libboris CUDA kernels, through the C ABI) vs the CPU oracle.
+
+Element-by-element parity at sizes that span several tiles/blocks plus a
+ragged tail; sampled parity at BASELINE full size; bit-exact invariants
+(AoS == SoA, aligned == unaligned, sharded == unsharded, mixed types == per-type
+runs, host-resident == device-resident, order/type/weight untouched).
+Tolerances: north_star (1e-12 fp64, 1e-5 fp32 after 100 steps) with the c15
+metric (tests/parity_util.py).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2104_04579_b200 as lb
+from paper_2104_04579_b200.ensemble import AosEnsemble, SoaEnsemble
+from parity_util import TOL, C15, OracleRun, rounded, stack3
+
+pytestmark = pytest.mark.gpu
+
+PREC = {"fp32": lb.BORIS_FP32, "fp64": lb.BORIS_FP64}
+LAYOUT = {"soa": lb.BORIS_LAYOUT_SOA, "aos": lb.BORIS_LAYOUT_AOS}
+N_SMALL = 3 * 4096 + 37        # several blocks / tiles + a ragged tail
+
+
+def gpu_field(w):
+    if w.field_kind == "uniform":
+        return lb.boris_field_create_uniform(w.uniform_E, w.uniform_B)
+    if w.field_kind == "plane_wave":
+        pw = w.plane_wave
+        return lb.boris_field_create_plane_wave(pw["E0"], pw["k_hat"], pw["e_hat"], pw["omega"],
+                                                pw["k"], pw["phase0"])
+    if w.field_kind == "mdipole":
+        md = w.plane_wave
+        return lb.boris_field_create_mdipole(md["A0"], md["omega0"], md["k"])
+    return None
+
+
+def build(w, layout, precision, n=None, host=False):
+    n = n or w.n
+    d = rounded(w.generate(0, n), precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    ens = cls(n, PREC[precision], w.types, w.light_velocity, host=host,
+              with_fields=w.field_kind == "arrays")
+    ens.fill(d)
+    ens.wrap()
+    field = ens.field if w.field_kind == "arrays" else gpu_field(w)
+    return d, ens, field
+
+
+def gpu_state(ens):
+    s = ens.state()
+    return (torch.stack([s["x"], s["y"], s["z"]], 1).numpy(),
+            torch.stack([s["px"], s["py"], s["pz"]], 1).numpy(), s["gamma"].numpy(), s)
+
+
+def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False):
+    d, ens, field = build(w, layout, precision, n, host=host)
+    ref = OracleRun(w, d, precision)
+    metric = C15()
+    done = 0
+    worst = {}
+    stream = torch.cuda.current_stream()
+    for s in checks:
+        k = s - done
+        lb.boris_push(ens.handle, field, w.dt, k, stream)
+        ref.push(k)
+        torch.cuda.synchronize()
+        done = s
+        r, p, g, st = gpu_state(ens)
+        er = metric("r", r, ref.pos)
+        ep = metric("p", p, ref.mom)
+        eg = float(np.max(np.abs(g - ref.gamma) / ref.gamma))
+        worst[s] = (er, ep, eg)
+        # order, types, weights untouched (bit-exact)
+        assert torch.equal(st["type"], d["type"].to(torch.int16))
+        assert torch.equal(st["weight"], d["weight"])
+    tol = TOL[precision]
+    for s, (er, ep, eg) in worst.items():
+        assert er <= tol and ep <= tol and eg <= tol, (s, worst)
+    assert lb.boris_ensemble_get_time(ens.handle) == pytest.approx(done * w.dt, rel=1e-15)
+    if w.field_kind != "arrays":
+        lb.boris_field_destroy(field)
+    ens.close()
+    return worst
+
+
+# ---------------------------------------------------------------------------
+# Per-particle ("precalculated") fields, streaming kernels: C2 recipe.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_C2_arrays_parity(layout, precision):
+    w = synth.config("C2")
+    worst = run_parity(w, layout, precision, N_SMALL)
+    print(layout, precision, worst)
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_multitype_arrays_parity(layout, precision):
+    w = synth.config("C2")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    run_parity(w, layout, precision, N_SMALL)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 255, 256, 257, 1023, 1025])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_small_and_ragged_sizes(n, layout):
+    w = synth.config("C2")
+    run_parity(w, layout, "fp64", n, checks=(1, 3))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_aos_equals_soa_bitwise(precision):
+    w = synth.config("C2")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    _, soa, fs = build(w, "soa", precision, N_SMALL)
+    _, aos, fa = build(w, "aos", precision, N_SMALL)
+    for _ in range(3):
+        lb.boris_push(soa.handle, fs, w.dt, 1)
+        lb.boris_push(aos.handle, fa, w.dt, 1)
+    torch.cuda.synchronize()
+    a, b = soa.state(), aos.state()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(a[k], b[k]), k
+
+
+def test_unaligned_equals_aligned_bitwise():
+    """Sliced tensors (4 B offset) take the scalar path; arithmetic is identical."""
+    w = synth.config("C2")
+    n = 4099
+    d = rounded(w.generate(0, n + 1), "fp32")
+    big = SoaEnsemble(n + 1, lb.BORIS_FP32, w.types, w.light_velocity)
+    big.fill(d)
+    ref = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity)
+    ref.fill({k: v[1:] for k, v in d.items()})
+    ref.wrap()
+    keys = ("x", "y", "z", "px", "py", "pz")
+    h = lb.boris_ensemble_wrap_soa(0, lb.BORIS_MEMORY_DEVICE, lb.BORIS_FP32, n,
+                                   *(big.t[k][1:].data_ptr() for k in keys),
+                                   big.t["weight"][1:].data_ptr(), big.t["gamma"][1:].data_ptr(),
+                                   None, w.types, w.light_velocity)
+    f = lb.boris_field_create_arrays_soa(h, *(big.t[k][1:].data_ptr()
+                                              for k in ("Ex", "Ey", "Ez", "Bx", "By", "Bz")))
+    lb.boris_push(h, f, w.dt, 2)
+    lb.boris_push(ref.handle, ref.field, w.dt, 2)
+    torch.cuda.synchronize()
+    for k in keys + ("gamma",):
+        assert torch.equal(big.t[k][1:], ref.t[k]), k
+    lb.boris_field_destroy(f)
+    lb.boris_ensemble_destroy(h)
+
+
+def test_sharded_equals_unsharded_bitwise():
+    """pushing contiguous shards separately == pushing the whole."""
+    from paper_2104_04579_b200.dist import shard_range
+    w = synth.config("C5", n=50_001)
+    d = rounded(w.generate(), "fp32")
+    whole = SoaEnsemble(w.n, lb.BORIS_FP32, w.types, w.light_velocity)
+    whole.fill(d)
+    whole.wrap()
+    lb.boris_push(whole.handle, whole.field, w.dt, 3)
+    world = 4
+    parts = []
+    for rank in range(world):
+        lo, hi = shard_range(w.n, rank, world)
+        # each shard generated from the global index, as a rank would
+        ds = rounded(w.generate(lo, hi - lo), "fp32")
+        e = SoaEnsemble(hi - lo, lb.BORIS_FP32, w.types, w.light_velocity)
+        e.fill(ds)
+        e.wrap()
+        lb.boris_push(e.handle, e.field, w.dt, 3)
+        parts.append(e)
+    torch.cuda.synchronize()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(torch.cat([p.t[k] for p in parts]), whole.t[k]), k
+
+
+def test_mixed_types_equal_per_type_runs_bitwise():
+    w = synth.config("C2")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    d, mixed, fm = build(w, "soa", "fp64", N_SMALL)
+    lb.boris_push(mixed.handle, fm, w.dt, 5)
+    torch.cuda.synchronize()
+    for j, tp in enumerate(w.types):
+        sel = d["type"] == j
+        dj = {k: v[sel] for k, v in d.items()}
+        dj["type"] = torch.zeros_like(dj["type"])
+        e = SoaEnsemble(int(sel.sum()), lb.BORIS_FP64, [tp], w.light_velocity)
+        e.fill(dj)
+        e.wrap()
+        lb.boris_push(e.handle, e.field, w.dt, 5)
+        torch.cuda.synchronize()
+        for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+            assert torch.equal(mixed.t[k][sel.cuda()], e.t[k]), (j, k)
+
+
+# ---------------------------------------------------------------------------
+# Analytic fields, register-fused kernels: C1, C3, C4 recipes and the m-dipole.
+# ---------------------------------------------------------------------------
+
+def test_C1_larmor_fp64_soa():
+    w = synth.config("C1")
+    worst = run_parity(w, "soa", "fp64", w.n)
+    print(worst)
+
+
+def test_C1_matches_discrete_closed_form():
+    """BASELINE configs[0]: GPU vs the exact discrete Boris orbit (no oracle)."""
+    w = synth.config("C1")
+    d, ens, field = build(w, "soa", "fp64")
+    lb.boris_push(ens.handle, field, w.dt, w.n_steps)
+    torch.cuda.synchronize()
+    r, p, g, _ = gpu_state(ens)
+    q, m = w.types[0]
+    c = w.light_velocity
+    B = w.uniform_B[2]
+    gamma = math.sqrt(2.0)
+    alpha = -2 * math.atan(q * B * w.dt / (2 * gamma * m * c))
+    u0 = stack3(d, "px", "py", "pz") / (m * c)
+    z0 = u0[:, 0] + 1j * u0[:, 1]
+    N = w.n_steps
+    e = np.exp(1j * alpha)
+    s = z0 * e * (1 - np.exp(1j * N * alpha)) / (1 - e)
+    zN = z0 * np.exp(1j * N * alpha)
+    r0 = stack3(d, "x", "y", "z")
+    cdt = c * w.dt / gamma
+    r_ref = r0 + np.stack([cdt * s.real, cdt * s.imag, N * cdt * u0[:, 2]], 1)
+    p_ref = np.stack([zN.real, zN.imag, u0[:, 2]], 1) * m * c
+    assert np.abs(p - p_ref).max() / (m * c) < 1e-12
+    assert np.abs(r - r_ref).max() / (c * w.dt) < 1e-10
+    lb.boris_field_destroy(field)
+
+
+@pytest.mark.parametrize("layout", ["aos", "soa"])
+def test_C3_crossed_fields_three_types_fp64(layout):
+    w = synth.config("C3")
+    run_parity(w, layout, "fp64", N_SMALL)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_C4_plane_wave_parity(precision, layout):
+    w = synth.config("C4")
+    worst = run_parity(w, layout, precision, N_SMALL, checks=(1, 2, 10, 100))
+    print(precision, layout, worst)
+
+
+def mdipole_workload():
+    # m-dipole at P = 0.1 PW (reading c12: A0 = k sqrt(3P/c)).
+    w = synth.config("C4")
+    k = synth.OMEGA0 / synth.C_LIGHT
+    P = 1e21  # erg/s
+    w.field_kind = "mdipole"
+    w.plane_wave = dict(A0=k * math.sqrt(3 * P / synth.C_LIGHT), omega0=synth.OMEGA0, k=k)
+    w.dt = synth.T0 / 3.0e4    # peak |B| ~ 247 m c w0/e: ~0.05 rad rotation per step
+    return w
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_mdipole_parity(precision):
+    w = mdipole_workload()
+    worst = run_parity(w, "soa", precision, N_SMALL, checks=(1, 2, 10, 100))
+    print(precision, worst)
+
+
+# ---------------------------------------------------------------------------
+# Diagnostics, upload/download, host-resident ensembles, edge cases.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_kinetic_energy_diag(precision, layout):
+    w = synth.config("C5", n=N_SMALL)
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    d, ens, field = build(w, layout, precision)
+    ref = OracleRun(w, d, precision)
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(ens.handle, field, w.dt, 2, diag.data_ptr())
+    ref.push(2)
+    torch.cuda.synchronize()
+    ke, cnt = diag.tolist()
+    assert cnt == w.n
+    ke_ref = ref.kinetic_energy()
+    assert ke == pytest.approx(ke_ref, rel=1e-12 if precision == "fp64" else 2e-6)
+    # deterministic: a second diagnostic of the same state is bitwise equal
+    d2 = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_kinetic_energy(ens.handle, d2.data_ptr())
+    d3 = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_kinetic_energy(ens.handle, d3.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(d2, d3)
+    assert d2[0].item() == pytest.approx(ke_ref, rel=1e-12 if precision == "fp64" else 2e-6)
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_upload_download_roundtrip(layout, precision):
+    w = synth.config("C3", n=10_007)
+    d = w.generate()
+    h = lb.boris_ensemble_create(0, LAYOUT[layout], PREC[precision], w.n, w.types, w.light_velocity)
+    pos = stack3(d, "x", "y", "z")
+    mom = stack3(d, "px", "py", "pz") + 1e-3 * synth.M_ELECTRON * synth.C_LIGHT
+    lb.boris_ensemble_upload(h, 0, w.n, pos, mom, d["weight"].numpy(), d["type"].numpy())
+    out = lb.boris_ensemble_download(h, 0, w.n)
+    cast = (lambda a: a.astype(np.float32).astype(np.float64)) if precision == "fp32" else (lambda a: a)
+    assert np.array_equal(out["pos"], cast(pos))
+    assert np.array_equal(out["mom"], cast(mom))
+    assert np.array_equal(out["type"], d["type"].numpy())
+    m = np.array([t[1] for t in w.types])[out["type"]]
+    g_ref = np.sqrt(1 + np.sum(mom ** 2, 1) / (m * w.light_velocity) ** 2)
+    np.testing.assert_allclose(out["gamma"], g_ref, rtol=1e-15 if precision == "fp64" else 1e-7)
+    # partial range
+    sub = lb.boris_ensemble_download(h, 17, 100)
+    assert np.array_equal(sub["pos"], out["pos"][17:117])
+    bad = d["type"].numpy().copy()
+    bad[5] = 3
+    with pytest.raises(lb.BorisError) as ei:
+        lb.boris_ensemble_upload(h, 0, w.n, pos, mom, None, bad)
+    assert ei.value.status == lb.BORIS_E_TYPE_OUT_OF_RANGE
+    lb.boris_ensemble_destroy(h)
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_host_resident_equals_device_bitwise(layout, monkeypatch):
+    monkeypatch.setenv("BORIS_HOST_CHUNK", "4096")  # several chunks through the pipeline
+    w = synth.config("C2")
+    _, dev, fdev = build(w, layout, "fp32", N_SMALL)
+    _, host, fhost = build(w, layout, "fp32", N_SMALL, host=True)
+    for _ in range(2):
+        lb.boris_push(dev.handle, fdev, w.dt, 1)
+        lb.boris_push(host.handle, fhost, w.dt, 1)
+    torch.cuda.synchronize()
+    a, b = dev.state(), host.state()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(a[k], b[k]), k
+
+
+def test_host_resident_analytic_multistep():
+    w = synth.config("C4")
+    run_parity(w, "soa", "fp64", N_SMALL, checks=(5, 20), host=True)
+
+
+def test_edge_cases_and_errors():
+    w = synth.config("C2")
+    # n = 0 ensembles and n_steps = 0 pushes are no-ops
+    e0 = SoaEnsemble(0, lb.BORIS_FP32, w.types, w.light_velocity).wrap()
+    lb.boris_push(e0.handle, e0.field, w.dt, 3)
+    diag = torch.full((2,), 7.0, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(e0.handle, e0.field, w.dt, 1, diag.data_ptr())
+    torch.cuda.synchronize()
+    assert diag.tolist() == [0.0, 0.0]
+    _, e, f = build(w, "soa", "fp32", 1000)
+    before = e.state()
+    lb.boris_push(e.handle, f, w.dt, 0)
+    torch.cuda.synchronize()
+    after = e.state()
+    assert all(torch.equal(before[k], after[k]) for k in before)
+    with pytest.raises(lb.BorisError) as ei:
+        lb.boris_push(e.handle, f, float("nan"), 1)
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
+    with pytest.raises(lb.BorisError) as ei:
+        lb.boris_push(e.handle, f, w.dt, -1)
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
+    # field arrays of another ensemble size -> mismatch
+    _, e2, f2 = build(w, "soa", "fp32", 999)
+    with pytest.raises(lb.BorisError) as ei:
+        lb.boris_push(e.handle, f2, w.dt, 1)
+    assert ei.value.status == lb.BORIS_E_MISMATCH
+    # type out of range at wrap
+    three = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    bad = SoaEnsemble(100, lb.BORIS_FP32, three, w.light_velocity)
+    bad.t["type"][50] = 3
+    with pytest.raises(lb.BorisError) as ei:
+        bad.wrap()
+    assert ei.value.status == lb.BORIS_E_TYPE_OUT_OF_RANGE
+    bad.t["type"][50] = -1
+    with pytest.raises(lb.BorisError):
+        bad.wrap()
+
+
+# ---------------------------------------------------------------------------
+# Full BASELINE sizes, in the launch configuration bench.py times: sampled parity.
+# ---------------------------------------------------------------------------
+
+def _sampled_full_size(name, layout, precision, n_steps, n=None, sample=20_000):
+    w = synth.config(name, n=n)
+    d, ens, field = build(w, layout, precision)
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(ens.handle, field, w.dt, n_steps, diag.data_ptr())
+    torch.cuda.synchronize()
+    assert diag[1].item() == w.n
+    idx = np.unique(np.r_[np.linspace(0, w.n - 1, sample).astype(np.int64), w.n - 1, w.n - 2])
+    ds = {k: v[idx] for k, v in d.items()}
+    ref = OracleRun(w, ds, precision)
+    ref.push(n_steps)
+    r, p, g, _ = gpu_state(ens)
+    metric = C15()
+    er = metric("r", r[idx], ref.pos)
+    ep = metric("p", p[idx], ref.mom)
+    assert er <= TOL[precision] and ep <= TOL[precision], (er, ep)
+    if w.field_kind != "arrays":
+        lb.boris_field_destroy(field)
+    ens.close()
+    return er, ep
+
+
+def test_full_size_C2_fp32_soa_sampled():
+    print(_sampled_full_size("C2", "soa", "fp32", 1))
+
+
+def test_full_size_C2_fp64_aos_sampled():
+    print(_sampled_full_size("C2", "aos", "fp64", 1))
+
+
+def test_full_size_C3_sampled():
+    print(_sampled_full_size("C3", "aos", "fp64", 100))
+
+
+def test_full_size_C4_sampled():
+    print(_sampled_full_size("C4", "soa", "fp32", 100))
