@@ -118,7 +118,7 @@ def cpu_baseline(workload, target_s=15.0, sample=1 << 21, threads=None):
     t0 = time.perf_counter()
     oracle.push(*args, E=E, B=B, dt=workload.dt, n_steps=1, n_threads=threads)
     t1 = time.perf_counter() - t0
-    steps = int(max(1, min(200, target_s / max(t1, 1e-6))))
+    steps = int(max(1, min(2000, target_s / max(t1, 1e-6))))
     t0 = time.perf_counter()
     oracle.push(*args, E=E, B=B, dt=workload.dt, n_steps=steps, n_threads=threads)
     el = time.perf_counter() - t0

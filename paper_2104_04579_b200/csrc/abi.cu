@@ -249,15 +249,20 @@ template <typename FP>
 Coefs<FP> make_coefs(const boris_ensemble *e, double dt) {
     Coefs<FP> co;
     memset(&co, 0, sizeof co);
-    co.cdt = (FP)(e->c * dt);
     co.n_types = e->n_types;
     for (int i = 0; i < e->n_types; ++i) {
         const double q = e->types[i].charge, m = e->types[i].mass;
         const double mc = m * e->c;
-        co.t[i].alpha = (FP)(q * dt / (2.0 * mc));  // eq. 9-10, 13 in u-form
-        co.t[i].inv_mc = (FP)(1.0 / mc);
-        co.t[i].mc = (FP)mc;
-        co.ke[i] = m * e->c * e->c;
+        // S = 2^k closest to 1/(mc): u = S p is exact in binary floating point
+        const double S = std::ldexp(1.0, -(int)std::lround(std::log2(mc)));
+        const double kappa = 1.0 / (S * mc);
+        co.t[i].aE = (FP)(S * q * dt / 2.0);          // eq. 9-10
+        co.t[i].alpha = (FP)(q * dt / (2.0 * mc));    // eq. 13
+        co.t[i].kappa2 = (FP)(kappa * kappa);         // eq. 5
+        co.t[i].cr = (FP)(dt / (S * m));              // eq. 7
+        co.t[i].S = (FP)S;
+        co.t[i].invS = (FP)(1.0 / S);
+        co.ke[i] = 1.0 / (S * S * m);                 // m c^2 kappa^2
     }
     return co;
 }

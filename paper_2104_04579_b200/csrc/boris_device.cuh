@@ -1,16 +1,24 @@
 // boris_device.cuh -- device-side building blocks of the B200 Boris pusher.
 //
 // The per-particle arithmetic is the paper's procedure (arXiv 2104.04579 §2,
-// PAPER.md L175-186) in the normalised momentum u = p/(mc) ("u-form"), which is
-// eq. 9, 12, 13, 10, 5, 7 multiplied through by 1/(mc):
-//   u^-  = u + alpha E                       alpha = q dt/(2 m c)      (eq. 9)
-//   g_n  = sqrt(1 + |u^-|^2)                                            (L162)
-//   t    = alpha B / g_n,  s = 2 t/(1 + |t|^2)                          (eq. 13)
+// PAPER.md L175-186) on a power-of-two scaled momentum u = S p, S = 2^k ~ 1/(mc)
+// chosen per type on the host, so that p <-> u conversions are EXACT (no
+// rounding bias accumulates step after step) while every intermediate stays
+// O(1) in fp32 for any unit system.  With kappa = 1/(S m c):
+//   u^-  = u + aE E                  aE = S q dt/2                      (eq. 9)
+//   g_n  = sqrt(1 + kappa^2 |u^-|^2)                                     (L162)
+//   t    = alpha B / g_n             alpha = q dt/(2 m c)                (eq. 13)
+//   s    = 2 t/(1 + |t|^2)
 //   u'   = u^- + u^- x t,  u^+ = u^- + u' x s                            (eq. 12)
-//   u    = u^+ + alpha E                                                 (eq. 10)
-//   g    = sqrt(1 + |u|^2),  r += (c dt / g) u                           (eq. 5, 7)
-// Storage keeps the paper's momentum p = m c u (L207-212).  The u-form keeps
-// every intermediate O(1) so fp32 never under/overflows in CGS or SI units.
+//   u    = u^+ + aE E                                                    (eq. 10)
+//   g    = sqrt(1 + kappa^2 |u|^2),  r += (cr / g) u,  cr = dt/(S m)     (eq. 5, 7)
+// which is eq. 9-13, 5, 7 multiplied through by S (the rotation is scale-free).
+//
+// Every operation is an explicit IEEE intrinsic (__fmul_rn, __fadd_rn,
+// __fmaf_rn, ...): the compiler can neither contract nor reorder them, so every
+// kernel variant (SoA vector / scalar tail / unaligned, AoS tiles, multi-type,
+// with or without diagnostics, device- or host-resident) produces bit-identical
+// results for the same particle.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,91 +32,111 @@ constexpr int kMaxTypes = 32;  // == BORIS_MAX_TYPES
 // cast to FP.
 template <typename FP>
 struct TypeCoef {
-    FP alpha;   // q dt / (2 m c)
-    FP inv_mc;  // 1 / (m c)
-    FP mc;      // m c
+    FP aE;      // S q dt / 2       E half kick in scaled units (eq. 9-10)
+    FP alpha;   // q dt / (2 m c)   t = alpha B / gamma_n (eq. 13)
+    FP kappa2;  // 1 / (S m c)^2    gamma = sqrt(1 + kappa2 |u|^2) (eq. 5)
+    FP cr;      // dt / (S m)       r += cr u / gamma (eq. 7)
+    FP S;       // 2^k              u = S p (exact)
+    FP invS;    // 2^-k             p = invS u (exact)
 };
 
 template <typename FP>
 struct Coefs {
-    FP cdt;       // c dt
     int n_types;  // table entries used
     TypeCoef<FP> t[kMaxTypes];
-    double ke[kMaxTypes];  // m c^2 for the kinetic-energy diagnostic
+    double ke[kMaxTypes];  // m c^2 kappa^2 = 1/(S^2 m): KE = w ke |u|^2/(gamma+1)
 };
 
 // ---------------------------------------------------------------------------
-// Correctly rounded elementary operations (IEEE round-to-nearest, reading c14).
+// Correctly rounded elementary operations (IEEE round-to-nearest, reading c14),
+// never contracted or reassociated by the compiler.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float b_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double b_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float b_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double b_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float b_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double b_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float b_sqrt(float x) { return __fsqrt_rn(x); }
 __device__ __forceinline__ double b_sqrt(double x) { return __dsqrt_rn(x); }
 __device__ __forceinline__ float b_rcp(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double b_rcp(double x) { return __drcp_rn(x); }
 
-// One Boris momentum update in u-form for one particle (steps a4-a9).
+// |v|^2 = fma(x, x, fma(y, y, z*z))
+template <typename FP>
+__device__ __forceinline__ FP b_norm2(FP x, FP y, FP z) {
+    return b_fma(x, x, b_fma(y, y, b_mul(z, z)));
+}
+// a*b - c*d (one component of a cross product)
+template <typename FP>
+__device__ __forceinline__ FP b_cross(FP a, FP b, FP c, FP d) {
+    return b_fma(a, b, -b_mul(c, d));
+}
+
+// One Boris momentum update on the scaled momentum u (steps a4-a9).
 // Returns 1/gamma^{n+1/2}; writes gamma^{n+1/2} to `gamma`.
 template <typename FP>
 __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP Ey, FP Ez, FP Bx,
-                                             FP By, FP Bz, FP alpha, FP &gamma) {
+                                             FP By, FP Bz, const TypeCoef<FP> &tc, FP &gamma) {
     // a4: first electric half kick (eq. 9)
-    const FP ex = alpha * Ex, ey = alpha * Ey, ez = alpha * Ez;
-    ux += ex;
-    uy += ey;
-    uz += ez;
+    const FP ex = b_mul(tc.aE, Ex), ey = b_mul(tc.aE, Ey), ez = b_mul(tc.aE, Ez);
+    ux = b_add(ux, ex);
+    uy = b_add(uy, ey);
+    uz = b_add(uz, ez);
     // a5: gamma_n = gamma(u^-) (L162, reading c2)
-    const FP gn = b_sqrt(FP(1) + (ux * ux + uy * uy + uz * uz));
+    const FP gn = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
     // a6: rotation vectors (eq. 13)
-    const FP ta = alpha * b_rcp(gn);
-    const FP tx = ta * Bx, ty = ta * By, tz = ta * Bz;
-    const FP sf = FP(2) * b_rcp(FP(1) + (tx * tx + ty * ty + tz * tz));
-    const FP sx = sf * tx, sy = sf * ty, sz = sf * tz;
+    const FP ta = b_mul(tc.alpha, b_rcp(gn));
+    const FP tx = b_mul(ta, Bx), ty = b_mul(ta, By), tz = b_mul(ta, Bz);
+    const FP sf = b_mul(FP(2), b_rcp(b_add(FP(1), b_norm2(tx, ty, tz))));
+    const FP sx = b_mul(sf, tx), sy = b_mul(sf, ty), sz = b_mul(sf, tz);
     // a7: rotation (eq. 12): u' = u^- + u^- x t ; u^+ = u^- + u' x s
-    const FP upx = ux + (uy * tz - uz * ty);
-    const FP upy = uy + (uz * tx - ux * tz);
-    const FP upz = uz + (ux * ty - uy * tx);
-    ux += upy * sz - upz * sy;
-    uy += upz * sx - upx * sz;
-    uz += upx * sy - upy * sx;
+    const FP upx = b_add(ux, b_cross(uy, tz, uz, ty));
+    const FP upy = b_add(uy, b_cross(uz, tx, ux, tz));
+    const FP upz = b_add(uz, b_cross(ux, ty, uy, tx));
+    ux = b_add(ux, b_cross(upy, sz, upz, sy));
+    uy = b_add(uy, b_cross(upz, sx, upx, sz));
+    uz = b_add(uz, b_cross(upx, sy, upy, sx));
     // a8: second electric half kick (eq. 10)
-    ux += ex;
-    uy += ey;
-    uz += ez;
+    ux = b_add(ux, ex);
+    uy = b_add(uy, ey);
+    uz = b_add(uz, ez);
     // a9: gamma^{n+1/2} (eq. 5, reading c3)
-    gamma = b_sqrt(FP(1) + (ux * ux + uy * uy + uz * uz));
+    gamma = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
     return b_rcp(gamma);
 }
 
 // One full Boris step of one particle on stored quantities (rows a1-a11):
-// p -> u, boris_momentum, position update, u -> p.  Shared by every streaming
-// path (SoA vector/scalar, AoS tiles) so they are bitwise identical.
+// p -> u (exact), boris_momentum, position update, u -> p (exact).  Shared by
+// every streaming path so they are bitwise identical.
 template <typename FP>
 __device__ __forceinline__ void push_one(FP &x, FP &y, FP &z, FP &px, FP &py, FP &pz, FP &g,
                                          FP Ex, FP Ey, FP Ez, FP Bx, FP By, FP Bz,
-                                         const TypeCoef<FP> &tc, FP cdt, FP &ux, FP &uy,
-                                         FP &uz) {
-    ux = px * tc.inv_mc;
-    uy = py * tc.inv_mc;
-    uz = pz * tc.inv_mc;
-    const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc.alpha, g);
-    // a10: r^{n+1} = r^n + (c dt / gamma) u^{n+1/2}   (eq. 7)
-    const FP ct = cdt * inv_g;
-    x += ct * ux;
-    y += ct * uy;
-    z += ct * uz;
-    // a11: store p = m c u
-    px = ux * tc.mc;
-    py = uy * tc.mc;
-    pz = uz * tc.mc;
+                                         const TypeCoef<FP> &tc, FP &ux, FP &uy, FP &uz) {
+    ux = b_mul(px, tc.S);
+    uy = b_mul(py, tc.S);
+    uz = b_mul(pz, tc.S);
+    const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, g);
+    // a10: r^{n+1} = r^n + dt p^{n+1/2}/(gamma m) = r^n + (cr/gamma) u   (eq. 7)
+    const FP ct = b_mul(tc.cr, inv_g);
+    x = b_fma(ct, ux, x);
+    y = b_fma(ct, uy, y);
+    z = b_fma(ct, uz, z);
+    // a11: store p = u / S
+    px = b_mul(ux, tc.invS);
+    py = b_mul(uy, tc.invS);
+    pz = b_mul(uz, tc.invS);
 }
 
-// Kinetic energy of one macroparticle, w m c^2 |u|^2 / (gamma + 1) (= w (gamma-1) m c^2
-// without cancellation, reading c17), accumulated in double.
+// Kinetic energy of one macroparticle, w m c^2 |p/(mc)|^2 / (gamma + 1)
+// (= w (gamma-1) m c^2 without cancellation, reading c17), in double;
+// ke = m c^2 kappa^2 converts |u|^2 to |p/(mc)|^2.
 template <typename FP>
 __device__ __forceinline__ double kinetic_energy(FP ux, FP uy, FP uz, FP gamma, FP w,
-                                                 double mc2) {
+                                                 double ke) {
     const double dux = ux, duy = uy, duz = uz;
-    const double u2 = dux * dux + duy * duy + duz * duz;
-    return (double)w * mc2 * u2 / ((double)gamma + 1.0);
+    const double u2 = __fma_rn(dux, dux, __fma_rn(duy, duy, __dmul_rn(duz, duz)));
+    return __ddiv_rn(__dmul_rn(__dmul_rn((double)w, ke), u2), __dadd_rn((double)gamma, 1.0));
 }
 
 // ---------------------------------------------------------------------------

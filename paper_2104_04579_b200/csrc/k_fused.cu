@@ -197,20 +197,21 @@ __global__ void __launch_bounds__(kFusedThreads)
         Particle<FP, LAYOUT>::load(e, i, x, y, z, px, py, pz, w, ty);
         if (!MULTI) ty = 0;
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
-        FP ux = px * tc.inv_mc, uy = py * tc.inv_mc, uz = pz * tc.inv_mc;
+        FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
         FP gam = FP(1);
         for (int64_t s = 0; s < n_steps; ++s) {
             FP Ex, Ey, Ez, Bx, By, Bz;
             analytic_field<FP, FIELD>(fa, x, y, z, s, Ex, Ey, Ez, Bx, By, Bz);
-            const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc.alpha, gam);
-            const FP ct = co.cdt * inv_g;
+            const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
+            const FP ct = b_mul(tc.cr, inv_g);
             // a10 (eq. 7) with the position accumulated in double
-            x += (double)(ct * ux);
-            y += (double)(ct * uy);
-            z += (double)(ct * uz);
+            x = __dadd_rn(x, (double)b_mul(ct, ux));
+            y = __dadd_rn(y, (double)b_mul(ct, uy));
+            z = __dadd_rn(z, (double)b_mul(ct, uz));
         }
-        if (n_steps == 0) gam = b_sqrt(FP(1) + (ux * ux + uy * uy + uz * uz));
-        Particle<FP, LAYOUT>::store(e, i, x, y, z, ux * tc.mc, uy * tc.mc, uz * tc.mc, gam);
+        if (n_steps == 0) gam = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
+        Particle<FP, LAYOUT>::store(e, i, x, y, z, b_mul(ux, tc.invS), b_mul(uy, tc.invS),
+                                    b_mul(uz, tc.invS), gam);
         if (DIAG) {
             ke += kinetic_energy<FP>(ux, uy, uz, gam, w, MULTI ? s_ke[ty] : co.ke[0]);
             cnt += 1.0;

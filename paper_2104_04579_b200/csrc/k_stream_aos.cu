@@ -96,7 +96,7 @@ __device__ __forceinline__ void push_record(unsigned char *rec, const FP *fld,
     const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
     FP ux, uy, uz, gam;
     push_one<FP>(r[0], r[1], r[2], r[3], r[4], r[5], gam, fld[0], fld[1], fld[2], fld[3], fld[4],
-                 fld[5], tc, co.cdt, ux, uy, uz);
+                 fld[5], tc, ux, uy, uz);
     r[7] = gam;
     if (DIAG) {
         ke += kinetic_energy<FP>(ux, uy, uz, gam, r[6], MULTI ? s_ke[ty] : co.ke[0]);

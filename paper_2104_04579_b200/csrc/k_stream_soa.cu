@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kStreamThreads)
             const TypeCoef<FP> tc = MULTI ? s_t[ty[j]] : co.t[0];
             FP ux, uy, uz;
             push_one<FP>(x.v[j], y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], gm.v[j], ex.v[j],
-                         ey.v[j], ez.v[j], bx.v[j], by.v[j], bz.v[j], tc, co.cdt, ux, uy, uz);
+                         ey.v[j], ez.v[j], bx.v[j], by.v[j], bz.v[j], tc, ux, uy, uz);
             if (DIAG) {
                 ke += kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j],
                                          MULTI ? s_ke[ty[j]] : co.ke[0]);
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kStreamThreads)
         FP ux, uy, uz, gam;
         FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
         push_one<FP>(x, y, z, px, py, pz, gam, EX[i], EY[i], EZ[i], BX[i], BY[i], BZ[i], tc,
-                     co.cdt, ux, uy, uz);
+                     ux, uy, uz);
         X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
         if (DIAG) {
             ke += kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1),
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kStreamThreads)
         FP ux, uy, uz, gam;
         FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
         push_one<FP>(x, y, z, px, py, pz, gam, EX[i], EY[i], EZ[i], BX[i], BY[i], BZ[i], tc,
-                     co.cdt, ux, uy, uz);
+                     ux, uy, uz);
         X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
         if (DIAG) {
             ke += kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1),

@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(kStreamThreads)
         }
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
         // gamma from p (eq. 5), so the diagnostic does not depend on a stored gamma
-        const FP ux = px * tc.inv_mc, uy = py * tc.inv_mc, uz = pz * tc.inv_mc;
-        g = b_sqrt(FP(1) + (ux * ux + uy * uy + uz * uz));
+        const FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
+        g = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
         ke += kinetic_energy<FP>(ux, uy, uz, g, w, MULTI ? s_ke[ty] : co.ke[0]);
         cnt += 1.0;
     }

@@ -1,9 +1,21 @@
+#!/bin/bash
+# One GPU session: smoke, GPU tests, default bench, ncu launch list + full capture.
+# Usage (from the repo root, under gpurun): bash scripts/gpu_check.sh [quick]
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
-timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
-tail -5 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --particles 100000000 --steps 20 --warmup 3 --e2e-steps 2 > gpurun_out/bench_1e8.json 2> gpurun_out/bench_1e8.err; echo bench rc=$?
-cat gpurun_out/bench_1e8.json
-tail -20 gpurun_out/bench_1e8.err
+timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+grep -E "passed|failed" gpurun_out/pytest_gpu.log | tail -3
+grep -E "^(FAILED|ERROR)" gpurun_out/pytest_gpu.log | head -20
+[ "$1" = "quick" ] && exit 0
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+cat gpurun_out/bench.json; tail -5 gpurun_out/bench.err
+NCU=/usr/local/cuda/bin/ncu
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"k_stream|k_diag|k_fused" -c 40 \
+  --csv --log-file gpurun_out/launches.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline \
+  > gpurun_out/launches_bench.log 2>&1; echo ncu-launches rc=$?
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_stream_soa_vec -s 3 -c 1 \
+  -o gpurun_out/prof_soa_1e8 -f python bench.py --particles 100000000 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline \
+  > gpurun_out/prof_soa.log 2>&1; echo ncu-full rc=$?
+tail -3 gpurun_out/prof_soa.log

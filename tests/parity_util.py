@@ -16,10 +16,11 @@ class C15:
     trajectory scale max_{s' <= s} rms_j ||x_ref,j(s')||."""
 
     def __init__(self):
-        self.scale = {"r": 0.0, "p": 0.0}
+        self.scale = {}
 
     def __call__(self, key, gpu, ref):
         nrm = np.linalg.norm(ref, axis=1)
+        self.scale.setdefault(key, 0.0)
         if nrm.size:
             self.scale[key] = max(self.scale[key], float(np.sqrt(np.mean(nrm ** 2))))
         s = self.scale[key] if self.scale[key] > 0 else 1.0
