@@ -231,6 +231,17 @@ boris_status boris_field_create_mdipole(double A0, double omega0, double k, bori
 
 boris_status boris_field_destroy(boris_field *field);
 
+/*
+ * "Precalculated fields" (L369-371, reading c6): evaluate the analytic field
+ * `analytic` (uniform / plane wave / m-dipole) at every particle's current
+ * position r_i at time t and write it into the per-particle field `out` (arrays
+ * created with boris_field_create_arrays_* for `ens`; layout, precision, n,
+ * device and residency must match, else MISMATCH).  The values are those the
+ * fused push would use at (r_i, t).  Device ensembles only.  Asynchronous.
+ */
+boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensemble *ens,
+                                  double t, const boris_field *out, void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* Push (paper §2)                        */
 /* ------------------------------------------------------------------------ */
@@ -249,7 +260,9 @@ boris_status boris_field_destroy(boris_field *field);
  * Asynchronous on `stream`; advances the ensemble time by n_steps*dt.
  *
  * Device ensembles: per-particle fields -> one streaming kernel launch per
- * step; analytic fields -> one register-fused launch for all n_steps.
+ * step when n_steps == 1, one register-fused launch otherwise (bitwise the
+ * same, see boris_push_ex); analytic fields -> one register-fused launch for
+ * all n_steps.
  * Host ensembles: the ensemble (and per-particle fields) stream through the
  * GPU in chunks with H2D / compute / D2H overlapped; each chunk is pushed all
  * n_steps while resident.  Host arrays must be pinned for asynchrony.
@@ -270,6 +283,27 @@ boris_status boris_push(boris_ensemble *ens, const boris_field *field, double dt
  */
 boris_status boris_push_diag(boris_ensemble *ens, const boris_field *field, double dt,
                              int64_t n_steps, double *d_diag, void *stream);
+
+/*
+ * Push flags for boris_push_ex.
+ * BORIS_PUSH_AUTO (0): per-particle fields with n_steps > 1 run register-fused
+ *   (E, B read once, the state kept in registers in FP and rounded exactly as
+ *   the streaming kernel stores it): bitwise identical to n_steps single steps,
+ *   with 1/n_steps of the HBM traffic.  boris_push / boris_push_diag use this.
+ * BORIS_PUSH_STREAM_EACH_STEP: one streaming launch per step, re-reading the
+ *   field array every step -- the paper's "precalculated fields" benchmark
+ *   semantics (L369-371, L497-500).  Same results, HBM-bound.
+ */
+#define BORIS_PUSH_AUTO 0u
+#define BORIS_PUSH_STREAM_EACH_STEP 1u
+
+/*
+ * boris_push / boris_push_diag with explicit flags (see above); d_diag may be
+ * NULL (no diagnostic) or a DEVICE buffer of 2 doubles as in boris_push_diag.
+ * Unknown flag bits: INVALID_ARG.
+ */
+boris_status boris_push_ex(boris_ensemble *ens, const boris_field *field, double dt,
+                           int64_t n_steps, uint32_t flags, double *d_diag, void *stream);
 
 /* The same diagnostic for the current state, without pushing (asynchronous);
  * gamma is recomputed from p (eq. 5), not read from the stored gamma. */

@@ -36,6 +36,8 @@ BORIS_FP64 = 1
 BORIS_MEMORY_DEVICE = 0
 BORIS_MEMORY_HOST = 1
 BORIS_MAX_TYPES = 32
+BORIS_PUSH_AUTO = 0
+BORIS_PUSH_STREAM_EACH_STEP = 1
 BORIS_AOS_RECORD_BYTES = {BORIS_FP32: 36, BORIS_FP64: 72}
 BORIS_AOS_FIELD_BYTES = {BORIS_FP32: 24, BORIS_FP64: 48}
 
@@ -47,7 +49,8 @@ EXPORTED = (
     "boris_ensemble_validate_types", "boris_ensemble_get_info", "boris_ensemble_get_time",
     "boris_ensemble_set_time", "boris_field_create_arrays_soa", "boris_field_create_arrays_aos",
     "boris_field_create_uniform", "boris_field_create_plane_wave", "boris_field_create_mdipole",
-    "boris_field_destroy", "boris_push", "boris_push_diag", "boris_kinetic_energy",
+    "boris_field_destroy", "boris_field_evaluate", "boris_push", "boris_push_diag", "boris_push_ex",
+    "boris_kinetic_energy",
 )
 
 
@@ -91,19 +94,23 @@ _SIGNATURES = {
     "boris_field_create_plane_wave": ([_d, _dp, _dp, _d, _d, _d, _hp], _i32),
     "boris_field_create_mdipole": ([_d, _d, _d, _hp], _i32),
     "boris_field_destroy": ([_vp], _i32),
+    "boris_field_evaluate": ([_vp, _vp, _d, _vp, _vp], _i32),
     "boris_push": ([_vp, _vp, _d, _i64, _vp], _i32),
     "boris_push_diag": ([_vp, _vp, _d, _i64, _vp, _vp], _i32),
+    "boris_push_ex": ([_vp, _vp, _d, _i64, ctypes.c_uint32, _vp, _vp], _i32),
     "boris_kinetic_energy": ([_vp, _vp, _vp], _i32),
 }
 
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
-    """Load libboris.so (raises ImportError if it is missing: no fallback exists)."""
+def load_library(path: str | None = None):
+    """Load libboris.so (raises ImportError if it is missing: no fallback exists).
+    LIBBORIS_PATH may point at a tuning variant built by `_build --tag`."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("LIBBORIS_PATH") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"libboris.so not found at {path}; build it with "
@@ -309,6 +316,11 @@ def boris_field_destroy(field):
     _check(load_library().boris_field_destroy(field), "boris_field_destroy")
 
 
+def boris_field_evaluate(analytic, ens, t, out, stream=None):
+    _check(load_library().boris_field_evaluate(analytic, ens, t, out, _stream(stream)),
+           "boris_field_evaluate")
+
+
 # ---------------------------------------------------------------------------
 # Push
 # ---------------------------------------------------------------------------
@@ -320,6 +332,11 @@ def boris_push(ens, field, dt, n_steps, stream=None):
 def boris_push_diag(ens, field, dt, n_steps, d_diag, stream=None):
     _check(load_library().boris_push_diag(ens, field, dt, n_steps, d_diag, _stream(stream)),
            "boris_push_diag")
+
+
+def boris_push_ex(ens, field, dt, n_steps, flags=BORIS_PUSH_AUTO, d_diag=None, stream=None):
+    _check(load_library().boris_push_ex(ens, field, dt, n_steps, flags, d_diag, _stream(stream)),
+           "boris_push_ex")
 
 
 def boris_kinetic_energy(ens, d_diag, stream=None):

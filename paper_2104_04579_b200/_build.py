@@ -52,17 +52,20 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> str:
+    """Build libboris.so, or with `tag` a variant build/libboris_<tag>.so compiled with
+    extra -D `defines` (tuning experiments; the product is always libboris.so)."""
     srcs = sources()
     hdrs = headers()
-    if not force and not _stale(LIB, srcs + hdrs + [__file__]):
-        return LIB
+    lib = LIB if not tag else os.path.join(BUILD_DIR, f"libboris_{tag}.so")
+    if not force and not _stale(lib, srcs + hdrs + [__file__]):
+        return lib
     os.makedirs(BUILD_DIR, exist_ok=True)
     cc = nvcc()
-    extra = ["-Xptxas", "-v"] if verbose else []
+    extra = (["-Xptxas", "-v"] if verbose else []) + [f"-D{d}" for d in defines]
 
     def compile_one(src):
-        obj = os.path.join(BUILD_DIR, os.path.basename(src) + ".o")
+        obj = os.path.join(BUILD_DIR, os.path.basename(src) + (f".{tag}" if tag else "") + ".o")
         if force or _stale(obj, [src] + hdrs + [__file__]):
             cmd = [cc] + NVCC_FLAGS + extra + ["-c", src, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -74,18 +77,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [cc] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--tag", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, defines=a.defines, tag=a.tag))

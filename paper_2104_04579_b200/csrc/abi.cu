@@ -262,7 +262,7 @@ Coefs<FP> make_coefs(const boris_ensemble *e, double dt) {
         co.t[i].cr = (FP)(dt / (S * m));              // eq. 7
         co.t[i].S = (FP)S;
         co.t[i].invS = (FP)(1.0 / S);
-        co.ke[i] = 1.0 / (S * S * m);                 // m c^2 kappa^2
+        co.t[i].ke = (FP)(1.0 / (S * S * m));         // m c^2 kappa^2
     }
     return co;
 }
@@ -300,9 +300,12 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
 template <typename FP>
 cudaError_t push_view(const boris_ensemble *e, const EnsView &v, const boris_field *f,
                       const FieldSoaPtrs &fs, const void *faos, double t0, double dt,
-                      int64_t n_steps, DiagOut *diag, cudaStream_t st) {
+                      int64_t n_steps, uint32_t flags, DiagOut *diag, cudaStream_t st) {
     const Coefs<FP> co = make_coefs<FP>(e, dt);
     if (f->kind == FK_ARRAYS) {
+        if (n_steps > 1 && !(flags & BORIS_PUSH_STREAM_EACH_STEP))
+            return launch_fused_arrays<FP>(v, fs, faos, co, n_steps, e->multi(), diag, e->device,
+                                           st);
         for (int64_t s = 0; s < n_steps; ++s) {
             DiagOut *d = (s == n_steps - 1) ? diag : nullptr;
             cudaError_t err = v.layout == BORIS_LAYOUT_SOA
@@ -398,7 +401,7 @@ boris_status ensure_pipeline(boris_ensemble *e, bool with_fields) {
 
 template <typename FP>
 boris_status push_host(boris_ensemble *e, const boris_field *f, double dt, int64_t n_steps,
-                       double *d_diag, cudaStream_t st) {
+                       uint32_t flags, double *d_diag, cudaStream_t st) {
     const bool arrays = f->kind == FK_ARRAYS;
     boris_status s = ensure_pipeline(e, arrays);
     if (s != BORIS_OK) return s;
@@ -469,7 +472,7 @@ boris_status push_host(boris_ensemble *e, const boris_field *f, double dt, int64
         FieldSoaPtrs fsp = {p->fsoa[b][0], p->fsoa[b][1], p->fsoa[b][2],
                             p->fsoa[b][3], p->fsoa[b][4], p->fsoa[b][5]};
         DiagOut diag = {e->partials, e->partials_cap, 0};
-        CUDA_TRY(push_view<FP>(e, v, f, fsp, p->faos[b], e->time, dt, n_steps,
+        CUDA_TRY(push_view<FP>(e, v, f, fsp, p->faos[b], e->time, dt, n_steps, flags,
                                d_diag ? &diag : nullptr, st),
                  "push kernel launch");
         if (d_diag)
@@ -979,13 +982,40 @@ boris_status boris_field_destroy(boris_field *f) {
     return ok();
 }
 
+boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensemble *e, double t,
+                                  const boris_field *out, void *stream) {
+    if (!analytic || !e || !out) return fail(BORIS_E_INVALID_ARG, "NULL argument");
+    if (analytic->kind == FK_ARRAYS)
+        return fail(BORIS_E_INVALID_ARG, "the source field must be analytic");
+    if (!std::isfinite(t)) return fail(BORIS_E_INVALID_ARG, "t must be finite");
+    if (out->kind != FK_ARRAYS || out->layout != e->layout || out->precision != e->precision ||
+        out->n != e->n || out->device != e->device || out->memory != e->memory)
+        return fail(BORIS_E_MISMATCH, "output field arrays do not match the ensemble");
+    if (e->memory != BORIS_MEMORY_DEVICE)
+        return fail(BORIS_E_UNSUPPORTED, "field evaluation needs a device-resident ensemble");
+    DeviceGuard g(e->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    cudaError_t err =
+        e->precision == BORIS_FP32
+            ? launch_field_evaluate<float>(e->view(), analytic->kind,
+                                           make_analytic<float>(analytic, t, 0.0), out->soa,
+                                           (void *)out->aos, e->device, (cudaStream_t)stream)
+            : launch_field_evaluate<double>(e->view(), analytic->kind,
+                                            make_analytic<double>(analytic, t, 0.0), out->soa,
+                                            (void *)out->aos, e->device, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "field evaluate launch");
+    return ok();
+}
+
 // ---------------------------------------------------------------------------
 // Push
 // ---------------------------------------------------------------------------
 static boris_status push_impl(boris_ensemble *e, const boris_field *f, double dt, int64_t n_steps,
-                              double *d_diag, cudaStream_t st) {
+                              uint32_t flags, double *d_diag, cudaStream_t st) {
     boris_status s = check_push_args(e, f, dt, n_steps);
     if (s != BORIS_OK) return s;
+    if (flags & ~(uint32_t)BORIS_PUSH_STREAM_EACH_STEP)
+        return fail(BORIS_E_INVALID_ARG, "unknown push flags 0x%x", flags);
     if (n_steps == 0 && !d_diag) return ok();
     DeviceGuard g(e->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
@@ -997,8 +1027,8 @@ static boris_status push_impl(boris_ensemble *e, const boris_field *f, double dt
             e->time += (double)n_steps * dt;
             return ok();
         }
-        s = e->precision == BORIS_FP32 ? push_host<float>(e, f, dt, n_steps, d_diag, st)
-                                       : push_host<double>(e, f, dt, n_steps, d_diag, st);
+        s = e->precision == BORIS_FP32 ? push_host<float>(e, f, dt, n_steps, flags, d_diag, st)
+                                       : push_host<double>(e, f, dt, n_steps, flags, d_diag, st);
         if (s != BORIS_OK) return s;
         e->time += (double)n_steps * dt;
         return ok();
@@ -1013,8 +1043,8 @@ static boris_status push_impl(boris_ensemble *e, const boris_field *f, double dt
                   : launch_kinetic_energy<double>(e->view(), make_coefs<double>(e, dt), e->multi(), dp, e->device, st);
     } else {
         err = e->precision == BORIS_FP32
-                  ? push_view<float>(e, e->view(), f, fs, f->aos, e->time, dt, n_steps, dp, st)
-                  : push_view<double>(e, e->view(), f, fs, f->aos, e->time, dt, n_steps, dp, st);
+                  ? push_view<float>(e, e->view(), f, fs, f->aos, e->time, dt, n_steps, flags, dp, st)
+                  : push_view<double>(e, e->view(), f, fs, f->aos, e->time, dt, n_steps, flags, dp, st);
     }
     if (err != cudaSuccess) return cuda_fail(err, "push kernel launch");
     if (d_diag) {
@@ -1031,13 +1061,18 @@ static boris_status push_impl(boris_ensemble *e, const boris_field *f, double dt
 
 boris_status boris_push(boris_ensemble *e, const boris_field *f, double dt, int64_t n_steps,
                         void *stream) {
-    return push_impl(e, f, dt, n_steps, nullptr, (cudaStream_t)stream);
+    return push_impl(e, f, dt, n_steps, BORIS_PUSH_AUTO, nullptr, (cudaStream_t)stream);
 }
 
 boris_status boris_push_diag(boris_ensemble *e, const boris_field *f, double dt, int64_t n_steps,
                              double *d_diag, void *stream) {
     if (!d_diag) return fail(BORIS_E_INVALID_ARG, "d_diag is NULL");
-    return push_impl(e, f, dt, n_steps, d_diag, (cudaStream_t)stream);
+    return push_impl(e, f, dt, n_steps, BORIS_PUSH_AUTO, d_diag, (cudaStream_t)stream);
+}
+
+boris_status boris_push_ex(boris_ensemble *e, const boris_field *f, double dt, int64_t n_steps,
+                           uint32_t flags, double *d_diag, void *stream) {
+    return push_impl(e, f, dt, n_steps, flags, d_diag, (cudaStream_t)stream);
 }
 
 boris_status boris_kinetic_energy(const boris_ensemble *e, double *d_diag, void *stream) {

@@ -38,13 +38,13 @@ struct TypeCoef {
     FP cr;      // dt / (S m)       r += cr u / gamma (eq. 7)
     FP S;       // 2^k              u = S p (exact)
     FP invS;    // 2^-k             p = invS u (exact)
+    FP ke;      // m c^2 kappa^2 = 1/(S^2 m): KE = w ke |u|^2/(gamma+1)
 };
 
 template <typename FP>
 struct Coefs {
     int n_types;  // table entries used
     TypeCoef<FP> t[kMaxTypes];
-    double ke[kMaxTypes];  // m c^2 kappa^2 = 1/(S^2 m): KE = w ke |u|^2/(gamma+1)
 };
 
 // ---------------------------------------------------------------------------
@@ -61,6 +61,31 @@ __device__ __forceinline__ float b_sqrt(float x) { return __fsqrt_rn(x); }
 __device__ __forceinline__ double b_sqrt(double x) { return __dsqrt_rn(x); }
 __device__ __forceinline__ float b_rcp(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double b_rcp(double x) { return __drcp_rn(x); }
+
+// Reciprocal square root and reciprocal used by the push.  Default (north_star:
+// "fp32 variants using rsqrt/FMA"): fp32 uses the MUFU approximations
+// rsqrt.approx / rcp.approx (<= 2 ulp); fp64 uses CUDA's rsqrt (1 ulp) and the
+// IEEE reciprocal.  -DBORIS_PRECISE_MATH switches every one of them to
+// correctly rounded sqrt + reciprocal.  Either way the operations are
+// deterministic, so all kernel variants stay bitwise identical.
+#ifdef BORIS_PRECISE_MATH
+__device__ __forceinline__ float b_rsqrt(float x) { return __frcp_rn(__fsqrt_rn(x)); }
+__device__ __forceinline__ double b_rsqrt(double x) { return __drcp_rn(__dsqrt_rn(x)); }
+__device__ __forceinline__ float b_rcpx(float x) { return __frcp_rn(x); }
+#else
+__device__ __forceinline__ float b_rsqrt(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ double b_rsqrt(double x) { return rsqrt(x); }
+__device__ __forceinline__ float b_rcpx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+#endif
+__device__ __forceinline__ double b_rcpx(double x) { return __drcp_rn(x); }
 
 // |v|^2 = fma(x, x, fma(y, y, z*z))
 template <typename FP>
@@ -83,12 +108,12 @@ __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP E
     ux = b_add(ux, ex);
     uy = b_add(uy, ey);
     uz = b_add(uz, ez);
-    // a5: gamma_n = gamma(u^-) (L162, reading c2)
-    const FP gn = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
+    // a5: 1/gamma_n, gamma_n = gamma(u^-) (L162, reading c2)
+    const FP inv_gn = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
     // a6: rotation vectors (eq. 13)
-    const FP ta = b_mul(tc.alpha, b_rcp(gn));
+    const FP ta = b_mul(tc.alpha, inv_gn);
     const FP tx = b_mul(ta, Bx), ty = b_mul(ta, By), tz = b_mul(ta, Bz);
-    const FP sf = b_mul(FP(2), b_rcp(b_add(FP(1), b_norm2(tx, ty, tz))));
+    const FP sf = b_mul(FP(2), b_rcpx(b_add(FP(1), b_norm2(tx, ty, tz))));
     const FP sx = b_mul(sf, tx), sy = b_mul(sf, ty), sz = b_mul(sf, tz);
     // a7: rotation (eq. 12): u' = u^- + u^- x t ; u^+ = u^- + u' x s
     const FP upx = b_add(ux, b_cross(uy, tz, uz, ty));
@@ -101,9 +126,16 @@ __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP E
     ux = b_add(ux, ex);
     uy = b_add(uy, ey);
     uz = b_add(uz, ez);
-    // a9: gamma^{n+1/2} (eq. 5, reading c3)
-    gamma = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
+    // a9: gamma^{n+1/2} (eq. 5, reading c3) and its reciprocal
+    const FP g2 = b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1));
+#ifdef BORIS_PRECISE_MATH
+    gamma = b_sqrt(g2);
     return b_rcp(gamma);
+#else
+    const FP inv_g = b_rsqrt(g2);
+    gamma = b_mul(g2, inv_g);
+    return inv_g;
+#endif
 }
 
 // One full Boris step of one particle on stored quantities (rows a1-a11):
@@ -129,14 +161,13 @@ __device__ __forceinline__ void push_one(FP &x, FP &y, FP &z, FP &px, FP &py, FP
 }
 
 // Kinetic energy of one macroparticle, w m c^2 |p/(mc)|^2 / (gamma + 1)
-// (= w (gamma-1) m c^2 without cancellation, reading c17), in double;
-// ke = m c^2 kappa^2 converts |u|^2 to |p/(mc)|^2.
+// (= w (gamma-1) m c^2 without cancellation, reading c17), evaluated in FP and
+// accumulated by the caller in double; tc.ke = m c^2 kappa^2 converts |u|^2.
 template <typename FP>
-__device__ __forceinline__ double kinetic_energy(FP ux, FP uy, FP uz, FP gamma, FP w,
-                                                 double ke) {
-    const double dux = ux, duy = uy, duz = uz;
-    const double u2 = __fma_rn(dux, dux, __fma_rn(duy, duy, __dmul_rn(duz, duz)));
-    return __ddiv_rn(__dmul_rn(__dmul_rn((double)w, ke), u2), __dadd_rn((double)gamma, 1.0));
+__device__ __forceinline__ FP kinetic_energy(FP ux, FP uy, FP uz, FP gamma, FP w,
+                                             const TypeCoef<FP> &tc) {
+    const FP u2 = b_norm2(ux, uy, uz);
+    return b_mul(b_mul(w, tc.ke), b_mul(u2, b_rcpx(b_add(gamma, FP(1)))));
 }
 
 // ---------------------------------------------------------------------------
@@ -275,12 +306,8 @@ __device__ __forceinline__ void block_diag_partial(double ke, double count, doub
 // Load the type table into shared memory (multi-type kernels).  Divergent
 // indexing into the kernel-parameter bank serialises; shared memory does not.
 template <typename FP>
-__device__ __forceinline__ void load_type_table(const Coefs<FP> &co, TypeCoef<FP> *s_t,
-                                                double *s_ke) {
-    for (int i = threadIdx.x; i < co.n_types; i += blockDim.x) {
-        s_t[i] = co.t[i];
-        s_ke[i] = co.ke[i];
-    }
+__device__ __forceinline__ void load_type_table(const Coefs<FP> &co, TypeCoef<FP> *s_t) {
+    for (int i = threadIdx.x; i < co.n_types; i += blockDim.x) s_t[i] = co.t[i];
     __syncthreads();
 }
 

@@ -77,6 +77,19 @@ cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP
                          const Coefs<FP> &co, int64_t n_steps, bool multi, DiagOut *diag,
                          int device, cudaStream_t st);
 
+// Analytic field at every particle's position (time baked into fa) -> arrays.
+template <typename FP>
+cudaError_t launch_field_evaluate(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
+                                  const FieldSoaPtrs &out, void *out_rec, int device,
+                                  cudaStream_t st);
+
+// n_steps in registers with per-particle (constant) fields; bitwise identical to
+// n_steps launches of the streaming kernels.
+template <typename FP>
+cudaError_t launch_fused_arrays(const EnsView &e, const FieldSoaPtrs &f, const void *frec,
+                                const Coefs<FP> &co, int64_t n_steps, bool multi,
+                                DiagOut *diag, int device, cudaStream_t st);
+
 template <typename FP>
 cudaError_t launch_kinetic_energy(const EnsView &e, const Coefs<FP> &co, bool multi,
                                   DiagOut *diag, int device, cudaStream_t st);

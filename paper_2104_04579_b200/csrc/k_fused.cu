@@ -186,8 +186,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
-    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
-    if (MULTI) load_type_table(co, s_t, s_ke);
+    if (MULTI) load_type_table(co, s_t);
     double ke = 0.0, cnt = 0.0;
     const int64_t stride = (int64_t)gridDim.x * kFusedThreads;
     for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride) {
@@ -213,7 +212,7 @@ __global__ void __launch_bounds__(kFusedThreads)
         Particle<FP, LAYOUT>::store(e, i, x, y, z, b_mul(ux, tc.invS), b_mul(uy, tc.invS),
                                     b_mul(uz, tc.invS), gam);
         if (DIAG) {
-            ke += kinetic_energy<FP>(ux, uy, uz, gam, w, MULTI ? s_ke[ty] : co.ke[0]);
+            ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, w, tc);
             cnt += 1.0;
         }
     }
@@ -289,5 +288,80 @@ template cudaError_t launch_fused<float>(const EnsView &, int, const AnalyticArg
 template cudaError_t launch_fused<double>(const EnsView &, int, const AnalyticArgs<double> &,
                                           const Coefs<double> &, int64_t, bool, DiagOut *, int,
                                           cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// "Precalculated fields": an analytic field evaluated at
+// every particle's current position at time t0 (fa built with that t0), written
+// to per-particle arrays (SoA) or {E,B} records (AoS).  Reads r (12/24 B),
+// writes E,B (24/48 B) per particle; same analytic_field as the fused push.
+// ---------------------------------------------------------------------------
+template <typename FP, int LAYOUT, int FIELD>
+__global__ void __launch_bounds__(kFusedThreads)
+    k_field_evaluate(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa, FieldSoaPtrs out,
+                     void *out_rec) {
+    const int64_t stride = (int64_t)gridDim.x * kFusedThreads;
+    for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride) {
+        double x, y, z;
+        FP px, py, pz, w;
+        int ty;
+        Particle<FP, LAYOUT>::load(e, i, x, y, z, px, py, pz, w, ty);
+        FP Ex, Ey, Ez, Bx, By, Bz;
+        analytic_field<FP, FIELD>(fa, x, y, z, 0, Ex, Ey, Ez, Bx, By, Bz);
+        if (LAYOUT == BORIS_LAYOUT_SOA) {
+            ((FP *)out.Ex)[i] = Ex;
+            ((FP *)out.Ey)[i] = Ey;
+            ((FP *)out.Ez)[i] = Ez;
+            ((FP *)out.Bx)[i] = Bx;
+            ((FP *)out.By)[i] = By;
+            ((FP *)out.Bz)[i] = Bz;
+        } else {
+            FP *r = (FP *)out_rec + 6 * i;
+            r[0] = Ex; r[1] = Ey; r[2] = Ez;
+            r[3] = Bx; r[4] = By; r[5] = Bz;
+        }
+    }
+}
+
+template <typename FP, int LAYOUT>
+static cudaError_t dispatch_eval(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
+                                 const FieldSoaPtrs &out, void *out_rec, int device,
+                                 cudaStream_t st) {
+    const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
+    const unsigned grid = (unsigned)stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads,
+                                                device);
+    switch (field_kind) {
+    case FK_UNIFORM:
+        k_field_evaluate<FP, LAYOUT, FK_UNIFORM><<<grid, kFusedThreads, 0, st>>>(e, fa, out, out_rec);
+        break;
+    case FK_PLANE_WAVE:
+        k_field_evaluate<FP, LAYOUT, FK_PLANE_WAVE><<<grid, kFusedThreads, 0, st>>>(e, fa, out, out_rec);
+        break;
+    case FK_MDIPOLE:
+        k_field_evaluate<FP, LAYOUT, FK_MDIPOLE><<<grid, kFusedThreads, 0, st>>>(e, fa, out, out_rec);
+        break;
+    default:
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+template <typename FP>
+cudaError_t launch_field_evaluate(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
+                                  const FieldSoaPtrs &out, void *out_rec, int device,
+                                  cudaStream_t st) {
+    if (e.n == 0) return cudaSuccess;
+    if (e.layout == BORIS_LAYOUT_SOA)
+        return dispatch_eval<FP, BORIS_LAYOUT_SOA>(e, field_kind, fa, out, out_rec, device, st);
+    return dispatch_eval<FP, BORIS_LAYOUT_AOS>(e, field_kind, fa, out, out_rec, device, st);
+}
+
+template cudaError_t launch_field_evaluate<float>(const EnsView &, int,
+                                                  const AnalyticArgs<float> &,
+                                                  const FieldSoaPtrs &, void *, int,
+                                                  cudaStream_t);
+template cudaError_t launch_field_evaluate<double>(const EnsView &, int,
+                                                   const AnalyticArgs<double> &,
+                                                   const FieldSoaPtrs &, void *, int,
+                                                   cudaStream_t);
 
 }  // namespace boris

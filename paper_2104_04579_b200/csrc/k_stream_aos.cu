@@ -89,8 +89,8 @@ struct AosGeom {
 // Push particle j of a shared-memory record tile (record layout of libboris.h).
 template <typename FP, bool MULTI, bool DIAG>
 __device__ __forceinline__ void push_record(unsigned char *rec, const FP *fld,
-                                            const Coefs<FP> &co, const TypeCoef<FP> *s_t,
-                                            const double *s_ke, double &ke, double &cnt) {
+                                            const Coefs<FP> &co, const TypeCoef<FP> *s_t, double &ke,
+                                            double &cnt) {
     FP *r = (FP *)rec;
     const int ty = MULTI ? *(const int16_t *)(rec + AosGeom<FP>::TYPE_OFF) : 0;
     const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
@@ -99,7 +99,7 @@ __device__ __forceinline__ void push_record(unsigned char *rec, const FP *fld,
                  fld[5], tc, ux, uy, uz);
     r[7] = gam;
     if (DIAG) {
-        ke += kinetic_energy<FP>(ux, uy, uz, gam, r[6], MULTI ? s_ke[ty] : co.ke[0]);
+        ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, r[6], tc);
         cnt += 1.0;
     }
 }
@@ -117,13 +117,12 @@ __global__ void __launch_bounds__(kAosThreads)
     unsigned char *s_fld = smem + Gm::STAGES * Gm::TILE_R;
     uint64_t *bar = (uint64_t *)(s_fld + Gm::STAGES * Gm::TILE_F);
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
-    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Gm::STAGES; ++s) mbar_init(&bar[s], 1);
         fence_proxy_async_smem();
     }
-    if (MULTI) load_type_table(co, s_t, s_ke);  // contains __syncthreads
+    if (MULTI) load_type_table(co, s_t);  // contains __syncthreads
     else __syncthreads();
 
     auto tile_count = [&](int64_t t) -> int {
@@ -155,7 +154,7 @@ __global__ void __launch_bounds__(kAosThreads)
         if ((int)threadIdx.x < c)
             push_record<FP, MULTI, DIAG>(s_rec + s * Gm::TILE_R + threadIdx.x * Gm::RB,
                                          (const FP *)(s_fld + s * Gm::TILE_F) + threadIdx.x * 6,
-                                         co, s_t, s_ke, ke, cnt);
+                                         co, s_t, ke, cnt);
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -172,7 +171,7 @@ __global__ void __launch_bounds__(kAosThreads)
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - n_main) {
         const int64_t i = n_main + threadIdx.x;
         push_record<FP, MULTI, DIAG>(rec + i * Gm::RB, (const FP *)(frec + i * Gm::FB), co, s_t,
-                                     s_ke, ke, cnt);
+                                     ke, cnt);
     }
     if (threadIdx.x == 0) bulk_wait_all();
     if (DIAG) block_diag_partial<kAosThreads>(ke, cnt, partials);

@@ -12,14 +12,17 @@
 
 namespace boris {
 
+#ifndef BORIS_STREAM_MINB
+#define BORIS_STREAM_MINB 1  // resident blocks per SM requested from ptxas (tuning knob)
+#endif
+
 template <typename FP, bool MULTI, bool DIAG>
-__global__ void __launch_bounds__(kStreamThreads)
+__global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
     k_stream_soa_vec(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ Coefs<FP> co,
                      int64_t n_groups, int64_t n, double *partials) {
     constexpr int V = Vec<FP>::N;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
-    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
-    if (MULTI) load_type_table(co, s_t, s_ke);
+    if (MULTI) load_type_table(co, s_t);
 
     FP *__restrict__ X = (FP *)s.x;
     FP *__restrict__ Y = (FP *)s.y;
@@ -71,8 +74,7 @@ __global__ void __launch_bounds__(kStreamThreads)
             push_one<FP>(x.v[j], y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], gm.v[j], ex.v[j],
                          ey.v[j], ez.v[j], bx.v[j], by.v[j], bz.v[j], tc, ux, uy, uz);
             if (DIAG) {
-                ke += kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j],
-                                         MULTI ? s_ke[ty[j]] : co.ke[0]);
+                ke += (double)kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j], tc);
                 cnt += 1.0;
             }
         }
@@ -95,8 +97,7 @@ __global__ void __launch_bounds__(kStreamThreads)
                      ux, uy, uz);
         X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
         if (DIAG) {
-            ke += kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1),
-                                     MULTI ? s_ke[s.type[i]] : co.ke[0]);
+            ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1), tc);
             cnt += 1.0;
         }
     }
@@ -110,8 +111,7 @@ __global__ void __launch_bounds__(kStreamThreads)
     k_stream_soa_scalar(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ Coefs<FP> co,
                         int64_t n, double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
-    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
-    if (MULTI) load_type_table(co, s_t, s_ke);
+    if (MULTI) load_type_table(co, s_t);
     FP *X = (FP *)s.x, *Y = (FP *)s.y, *Z = (FP *)s.z;
     FP *PX = (FP *)s.px, *PY = (FP *)s.py, *PZ = (FP *)s.pz, *G = (FP *)s.g;
     const FP *W = (const FP *)s.w;
@@ -128,8 +128,7 @@ __global__ void __launch_bounds__(kStreamThreads)
                      ux, uy, uz);
         X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
         if (DIAG) {
-            ke += kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1),
-                                     MULTI ? s_ke[ty] : co.ke[0]);
+            ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1), tc);
             cnt += 1.0;
         }
     }

@@ -30,8 +30,7 @@ template <typename FP, int LAYOUT, bool MULTI>
 __global__ void __launch_bounds__(kStreamThreads)
     k_kinetic_energy(EnsView e, const __grid_constant__ Coefs<FP> co, double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
-    __shared__ double s_ke[MULTI ? kMaxTypes : 1];
-    if (MULTI) load_type_table(co, s_t, s_ke);
+    if (MULTI) load_type_table(co, s_t);
     double ke = 0.0, cnt = 0.0;
     const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
     for (int64_t i = (int64_t)blockIdx.x * kStreamThreads + threadIdx.x; i < e.n; i += stride) {
@@ -54,7 +53,7 @@ __global__ void __launch_bounds__(kStreamThreads)
         // gamma from p (eq. 5), so the diagnostic does not depend on a stored gamma
         const FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
         g = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
-        ke += kinetic_energy<FP>(ux, uy, uz, g, w, MULTI ? s_ke[ty] : co.ke[0]);
+        ke += (double)kinetic_energy<FP>(ux, uy, uz, g, w, tc);
         cnt += 1.0;
     }
     block_diag_partial<kStreamThreads>(ke, cnt, partials);

@@ -86,7 +86,8 @@ def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False):
         assert np.all(dg <= TOL[precision] * (u_ref + s_u) + 2 * ulp), (s, float(dg.max()))
         eg = float(np.max(dg / (u_ref + s_u)))
         g_of_p = np.sqrt(1.0 + np.sum(p * p, 1) / (m * w.light_velocity) ** 2)
-        assert np.max(np.abs(g - g_of_p) / g_of_p) <= (4e-7 if precision == "fp32" else 4e-15)
+        # gamma = g2 * rsqrt(g2) with the <= 2 ulp MUFU rsqrt in fp32 (boris_device.cuh)
+        assert np.max(np.abs(g - g_of_p) / g_of_p) <= (1e-6 if precision == "fp32" else 4e-15)
         worst[s] = (er, ep, eg)
         # order, types, weights untouched (bit-exact)
         assert torch.equal(st["type"], d["type"].to(torch.int16))
@@ -194,6 +195,32 @@ def test_sharded_equals_unsharded_bitwise():
     torch.cuda.synchronize()
     for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
         assert torch.equal(torch.cat([p.t[k] for p in parts]), whole.t[k]), k
+
+
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fused_arrays_equal_streaming_each_step_bitwise(layout, precision):
+    """BORIS_PUSH_AUTO fuses n_steps with per-particle fields in registers; it must
+    equal n_steps streaming launches (BORIS_PUSH_STREAM_EACH_STEP) bit for bit,
+    diagnostic included."""
+    w = synth.config("C5")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    _, a, fa = build(w, layout, precision, N_SMALL)
+    _, b, fb = build(w, layout, precision, N_SMALL)
+    da = torch.zeros(2, dtype=torch.float64, device="cuda")
+    db = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_ex(a.handle, fa, w.dt, 7, lb.BORIS_PUSH_AUTO, da.data_ptr())
+    lb.boris_push_ex(b.handle, fb, w.dt, 7, lb.BORIS_PUSH_STREAM_EACH_STEP, db.data_ptr())
+    torch.cuda.synchronize()
+    sa, sb = a.state(), b.state()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma", "weight", "type"):
+        assert torch.equal(sa[k], sb[k]), k
+    assert da[1].item() == db[1].item() == N_SMALL
+    assert da[0].item() == pytest.approx(db[0].item(), rel=1e-14)
+    with pytest.raises(lb.BorisError) as ei:
+        lb.boris_push_ex(a.handle, fa, w.dt, 1, 0x80)
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
 
 
 def test_mixed_types_equal_per_type_runs_bitwise():
