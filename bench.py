@@ -198,9 +198,13 @@ def main():
     from paper_2104_04579_b200 import dist as bdist
     from paper_2104_04579_b200.ensemble import SoaEnsemble
 
-    rank, world = bdist.init("nccl")
+    # one process per GPU; BORIS_DIST_BACKEND=gloo + BORIS_SHARE_GPU=1 lets a 1-GPU box run
+    # the N>1 code path (all ranks on cuda:0) for testing -- never for a reported number.
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("BORIS_SHARE_GPU") == "1":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    rank, world = bdist.init(os.environ.get("BORIS_DIST_BACKEND", "nccl"))
     dev = torch.device("cuda", local)
     lb.load_library()
 

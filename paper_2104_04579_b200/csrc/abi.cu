@@ -276,9 +276,13 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
         a.B[i] = (FP)f->B[i];
     }
     if (f->kind == FK_PLANE_WAVE) {
-        for (int i = 0; i < 3; ++i) a.kvec[i] = f->k * f->k_hat[i];
+        for (int i = 0; i < 3; ++i) {
+            a.kvec[i] = f->k * f->k_hat[i];
+            a.kf[i] = (FP)a.kvec[i];
+        }
         a.ph0 = f->phase0 - f->omega * t0;
         a.wdt = f->omega * dt;
+        a.wdtf = (FP)a.wdt;
         const double *kh = f->k_hat, *eh = f->e_hat;
         const double kxe[3] = {kh[1] * eh[2] - kh[2] * eh[1], kh[2] * eh[0] - kh[0] * eh[2],
                                kh[0] * eh[1] - kh[1] * eh[0]};
@@ -290,6 +294,8 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
         a.A0 = (FP)f->A0;
         a.k = (FP)f->kd;
         a.k2 = (FP)(f->kd * f->kd);
+        a.A0k2 = (FP)(2.0 * f->A0 * f->kd);
+        a.mA02 = (FP)(-2.0 * f->A0);
         a.w0t0 = f->omega0 * t0;
         a.w0dt = f->omega0 * dt;
     }

@@ -38,8 +38,12 @@ struct AnalyticArgs {
     double wdt;      // omega * dt
     FP cE[3];        // E0 * e_hat
     FP cB[3];        // E0 * (k_hat x e_hat)
+    FP kf[3];        // kvec in FP (phase increments inside a fused window)
+    FP wdtf;         // omega * dt in FP
     // m-dipole (eq. 14-15, readings c9-c13): time phase w0 t_n = w0t0 + n * w0dt
     FP A0, k, k2;
+    FP A0k2;         // 2 A0 k
+    FP mA02;         // -2 A0
     double w0t0, w0dt;
 };
 

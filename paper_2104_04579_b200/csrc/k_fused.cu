@@ -39,6 +39,23 @@ __device__ __forceinline__ void sincos_fp(double a, float *s, float *c) {
     sincosf((float)r, s, c);
 }
 
+// phi mod 2 pi in [-pi, pi] (Cody-Waite, exact for |phi| < 2^40).
+__device__ __forceinline__ double reduce_2pi(double phi) {
+    const double q = rint(phi * kInvTwoPi);
+    return fma(-q, kTwoPiLo, fma(-q, kTwoPiHi, phi));
+}
+
+// cos of a phase within a few radians of [-pi, pi]: fp32 -> MUFU cos (abs error
+// ~2^-21, below the fp32 rounding of the phase itself) unless BORIS_PRECISE_MATH.
+__device__ __forceinline__ float cos_small(float x) {
+#ifdef BORIS_PRECISE_MATH
+    return cosf(x);
+#else
+    return __cosf(x);
+#endif
+}
+__device__ __forceinline__ double cos_small(double x) { return cos(x); }
+
 // m-dipole radial functions (eq. 15, readings c11, c13): g1 = f1/xi, g2 = f2/xi^2, f3.
 // Taylor coefficients generated at compile time from their defining series:
 //   j0 = sum (-1)^n xi^{2n}/(2n+1)!,  j1/xi = sum (-1)^n 2(n+1) xi^{2n}/(2n+3)!,
@@ -181,33 +198,94 @@ struct Particle {
 
 }  // namespace
 
+// The fused step loop runs in windows of kFlush steps.  At each window start the
+// position anchor r_a (fp64) absorbs the FP displacement accumulated in the
+// window (fp32: position effectively kept in fp64, reading c-fp32r, without an
+// fp64 op in the inner loop), and the plane-wave phase is re-anchored in fp64
+// and reduced mod 2 pi; inside the window
+//   phi_n = phi_a + kvec . (r - r_a) - (n - n_a) omega dt      (FP, |.| <~ pi + 0.5)
+// which is phi = k (k_hat . r^n) - omega t_n + phase0 (reading c5) re-associated.
+constexpr int kFlush = 8;
+// m-dipole: sin/cos(omega0 t_n) is the same for every particle; each block
+// tabulates it (fp64 sincos, cast to FP) once per launch in shared memory.
+// Launches are split into chunks of kTimeTab steps on the host.
+constexpr int kTimeTab = 1024;
+
 template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG>
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    __shared__ FP s_sin[FIELD == FK_MDIPOLE ? kTimeTab : 1];
+    __shared__ FP s_cos[FIELD == FK_MDIPOLE ? kTimeTab : 1];
     if (MULTI) load_type_table(co, s_t);
+    if constexpr (FIELD == FK_MDIPOLE) {
+        for (int j = threadIdx.x; j < n_steps; j += kFusedThreads) {
+            double sn, cs;
+            sincos(fa.w0t0 + (double)j * fa.w0dt, &sn, &cs);  // t_j = t0 + j dt (c5)
+            s_sin[j] = (FP)sn;
+            s_cos[j] = (FP)cs;
+        }
+        __syncthreads();
+    }
     double ke = 0.0, cnt = 0.0;
     const int64_t stride = (int64_t)gridDim.x * kFusedThreads;
     for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride) {
-        double x, y, z;
+        double xa, ya, za;
         FP px, py, pz, w;
         int ty;
-        Particle<FP, LAYOUT>::load(e, i, x, y, z, px, py, pz, w, ty);
+        Particle<FP, LAYOUT>::load(e, i, xa, ya, za, px, py, pz, w, ty);
         if (!MULTI) ty = 0;
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
         FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
         FP gam = FP(1);
-        for (int64_t s = 0; s < n_steps; ++s) {
-            FP Ex, Ey, Ez, Bx, By, Bz;
-            analytic_field<FP, FIELD>(fa, x, y, z, s, Ex, Ey, Ez, Bx, By, Bz);
-            const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
-            const FP ct = b_mul(tc.cr, inv_g);
-            // a10 (eq. 7) with the position accumulated in double
-            x = __dadd_rn(x, (double)b_mul(ct, ux));
-            y = __dadd_rn(y, (double)b_mul(ct, uy));
-            z = __dadd_rn(z, (double)b_mul(ct, uz));
+        for (int64_t s0 = 0; s0 < n_steps; s0 += kFlush) {
+            FP phia = FP(0);
+            if constexpr (FIELD == FK_PLANE_WAVE)
+                phia = (FP)reduce_2pi(fma(fa.kvec[0], xa, fma(fa.kvec[1], ya, fa.kvec[2] * za)) +
+                                      (fa.ph0 - (double)s0 * fa.wdt));
+            FP dx = FP(0), dy = FP(0), dz = FP(0);
+            const int m = (n_steps - s0) < kFlush ? (int)(n_steps - s0) : kFlush;
+            for (int j = 0; j < m; ++j) {
+                FP Ex, Ey, Ez, Bx, By, Bz;
+                if constexpr (FIELD == FK_UNIFORM) {
+                    Ex = fa.E[0]; Ey = fa.E[1]; Ez = fa.E[2];
+                    Bx = fa.B[0]; By = fa.B[1]; Bz = fa.B[2];
+                } else if constexpr (FIELD == FK_PLANE_WAVE) {
+                    const FP phi = b_fma(fa.kf[0], dx, b_fma(fa.kf[1], dy, b_fma(fa.kf[2], dz,
+                                   b_fma(-(FP)j, fa.wdtf, phia))));
+                    const FP c = cos_small(phi);
+                    Ex = b_mul(fa.cE[0], c); Ey = b_mul(fa.cE[1], c); Ez = b_mul(fa.cE[2], c);
+                    Bx = b_mul(fa.cB[0], c); By = b_mul(fa.cB[1], c); Bz = b_mul(fa.cB[2], c);
+                } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
+                    const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
+                    const FP R = b_sqrt(b_norm2(x, y, z));
+                    FP g1, g2, f3;
+                    md_radial<FP>(b_mul(fa.k, R), g1, g2, f3);
+                    const FP swt = s_sin[s0 + j], cwt = s_cos[s0 + j];
+                    const FP ce = b_mul(b_mul(fa.A0k2, cwt), g1);  // 2 A0 k cos(w t) f1/xi
+                    const FP sb = b_mul(fa.mA02, swt);              // -2 A0 sin(w t)
+                    const FP k2g2 = b_mul(fa.k2, g2);               // f2/R^2
+                    Ex = -b_mul(ce, y);
+                    Ey = b_mul(ce, x);
+                    Ez = FP(0);
+                    const FP sk = b_mul(sb, k2g2);
+                    Bx = b_mul(b_mul(sk, x), z);
+                    By = b_mul(b_mul(sk, y), z);
+                    Bz = b_mul(sb, b_fma(k2g2, b_mul(z, z), f3));
+                }
+                const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
+                // a10 (eq. 7): displacement accumulated in the window
+                const FP ct = b_mul(tc.cr, inv_g);
+                dx = b_fma(ct, ux, dx);
+                dy = b_fma(ct, uy, dy);
+                dz = b_fma(ct, uz, dz);
+            }
+            xa = __dadd_rn(xa, (double)dx);
+            ya = __dadd_rn(ya, (double)dy);
+            za = __dadd_rn(za, (double)dz);
         }
+        const double x = xa, y = ya, z = za;
         if (n_steps == 0) gam = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
         Particle<FP, LAYOUT>::store(e, i, x, y, z, b_mul(ux, tc.invS), b_mul(uy, tc.invS),
                                     b_mul(uz, tc.invS), gam);
@@ -275,11 +353,23 @@ cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP
         if (diag) diag->written = 0;
         return cudaSuccess;
     }
-    if (e.layout == BORIS_LAYOUT_SOA)
-        return dispatch_fused_field<FP, BORIS_LAYOUT_SOA>(e, field_kind, fa, co, n_steps, multi,
-                                                          diag, device, st);
-    return dispatch_fused_field<FP, BORIS_LAYOUT_AOS>(e, field_kind, fa, co, n_steps, multi,
-                                                      diag, device, st);
+    // m-dipole launches cover at most kTimeTab steps (the per-block time table);
+    // chunk c starts at t0 + c0 dt, omega0 t computed from the step index (c5).
+    const int64_t chunk = field_kind == FK_MDIPOLE ? kTimeTab : n_steps;
+    for (int64_t c0 = 0; c0 < n_steps; c0 += chunk) {
+        const int64_t m = (n_steps - c0) < chunk ? n_steps - c0 : chunk;
+        AnalyticArgs<FP> fc = fa;
+        fc.w0t0 = fa.w0t0 + (double)c0 * fa.w0dt;
+        DiagOut *d = (c0 + m == n_steps) ? diag : nullptr;
+        const cudaError_t err =
+            e.layout == BORIS_LAYOUT_SOA
+                ? dispatch_fused_field<FP, BORIS_LAYOUT_SOA>(e, field_kind, fc, co, m, multi, d,
+                                                             device, st)
+                : dispatch_fused_field<FP, BORIS_LAYOUT_AOS>(e, field_kind, fc, co, m, multi, d,
+                                                             device, st);
+        if (err != cudaSuccess) return err;
+    }
+    return cudaSuccess;
 }
 
 template cudaError_t launch_fused<float>(const EnsView &, int, const AnalyticArgs<float> &,

@@ -61,7 +61,8 @@ def max_over_ranks(value: float, device=None) -> float:
 
 def barrier(device=None):
     if dist.is_initialized() and dist.get_world_size() > 1:
-        if device is not None and torch.device(device).type == "cuda":
+        if (device is not None and torch.device(device).type == "cuda"
+                and dist.get_backend() == "nccl"):
             dist.barrier(device_ids=[torch.device(device).index or 0])
         else:
             dist.barrier()

@@ -312,6 +312,50 @@ def test_mdipole_parity(precision):
     print(precision, worst)
 
 
+@pytest.mark.parametrize("kind", ["uniform", "plane_wave", "mdipole"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_field_evaluate_vs_oracle(kind, precision, layout):
+    """boris_field_evaluate (precalculated fields, L369-371) == the oracle's field at
+    each particle's position and time t."""
+    w = mdipole_workload() if kind == "mdipole" else synth.config("C4" if kind == "plane_wave"
+                                                                   else "C3")
+    n = N_SMALL
+    d = rounded(w.generate(0, n), precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    ens = cls(n, PREC[precision], w.types, w.light_velocity, with_fields=True)
+    ens.fill(d)
+    ens.wrap()
+    src = gpu_field(w)
+    t = 0.37 * synth.T0
+    lb.boris_field_evaluate(src, ens.handle, t, ens.field)
+    torch.cuda.synchronize()
+    if layout == "soa":
+        E = torch.stack([ens.t[k].double().cpu() for k in ("Ex", "Ey", "Ez")], 1).numpy()
+        B = torch.stack([ens.t[k].double().cpu() for k in ("Bx", "By", "Bz")], 1).numpy()
+    else:
+        f = ens.fld.double().cpu().numpy()
+        E, B = f[:, :3], f[:, 3:]
+    from parity_util import oracle_field
+    okind, params = oracle_field(w, precision)
+    pos = stack3(d, "x", "y", "z")
+    Er = np.zeros_like(pos)
+    Br = np.zeros_like(pos)
+    for i in range(n):
+        if okind == oracle.FIELD_UNIFORM:
+            Er[i], Br[i] = params[:3], params[3:]
+        elif okind == oracle.FIELD_PLANE_WAVE:
+            Er[i], Br[i] = oracle.field_plane_wave(params, pos[i], t)
+        else:
+            Er[i], Br[i] = oracle.field_mdipole(params, pos[i], t)
+    scale = max(np.abs(Er).max(), np.abs(Br).max())
+    tol = 2e-6 if precision == "fp32" else 1e-13
+    assert np.abs(E - Er).max() <= tol * scale
+    assert np.abs(B - Br).max() <= tol * scale
+    lb.boris_field_destroy(src)
+    ens.close()
+
+
 # ---------------------------------------------------------------------------
 # Diagnostics, upload/download, host-resident ensembles, edge cases.
 # ---------------------------------------------------------------------------
