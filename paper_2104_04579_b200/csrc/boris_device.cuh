@@ -98,6 +98,56 @@ __device__ __forceinline__ FP b_cross(FP a, FP b, FP c, FP d) {
     return b_fma(a, b, -b_mul(c, d));
 }
 
+// Steps a6 (s from t, eq. 13) and a7 (rotation, eq. 12) given t.
+template <typename FP>
+__device__ __forceinline__ void boris_rotate(FP &ux, FP &uy, FP &uz, FP tx, FP ty, FP tz) {
+    const FP sf = b_mul(FP(2), b_rcpx(b_add(FP(1), b_norm2(tx, ty, tz))));
+    const FP sx = b_mul(sf, tx), sy = b_mul(sf, ty), sz = b_mul(sf, tz);
+    // u' = u^- + u^- x t ; u^+ = u^- + u' x s
+    const FP upx = b_add(ux, b_cross(uy, tz, uz, ty));
+    const FP upy = b_add(uy, b_cross(uz, tx, ux, tz));
+    const FP upz = b_add(uz, b_cross(ux, ty, uy, tx));
+    ux = b_add(ux, b_cross(upy, sz, upz, sy));
+    uy = b_add(uy, b_cross(upz, sx, upx, sz));
+    uz = b_add(uz, b_cross(upx, sy, upy, sx));
+}
+
+// Step a9: gamma^{n+1/2} (eq. 5, reading c3); returns its reciprocal.
+template <typename FP>
+__device__ __forceinline__ FP boris_gamma(FP ux, FP uy, FP uz, FP kappa2, FP &gamma) {
+    const FP g2 = b_fma(kappa2, b_norm2(ux, uy, uz), FP(1));
+#ifdef BORIS_PRECISE_MATH
+    gamma = b_sqrt(g2);
+    return b_rcp(gamma);
+#else
+    const FP inv_g = b_rsqrt(g2);
+    gamma = b_mul(g2, inv_g);
+    return inv_g;
+#endif
+}
+
+// Boris momentum update for a field of fixed directions with a common scalar
+// amplitude c: E = c e, B = c b (plane wave: c = cos phi; uniform: c = 1, UNIT).
+// ae = aE e and ab = alpha b are precomputed per particle (per type), which
+// saves 6 multiplies per step in the register-fused kernels.  Same steps a4-a9.
+template <typename FP, bool UNIT>
+__device__ __forceinline__ FP boris_momentum_dir(FP &ux, FP &uy, FP &uz, FP c, const FP (&ae)[3],
+                                                 const FP (&ab)[3], FP kappa2, FP &gamma) {
+    const FP ex = UNIT ? ae[0] : b_mul(c, ae[0]);
+    const FP ey = UNIT ? ae[1] : b_mul(c, ae[1]);
+    const FP ez = UNIT ? ae[2] : b_mul(c, ae[2]);
+    ux = b_add(ux, ex);
+    uy = b_add(uy, ey);
+    uz = b_add(uz, ez);
+    const FP inv_gn = b_rsqrt(b_fma(kappa2, b_norm2(ux, uy, uz), FP(1)));
+    const FP ta = UNIT ? inv_gn : b_mul(inv_gn, c);
+    boris_rotate<FP>(ux, uy, uz, b_mul(ta, ab[0]), b_mul(ta, ab[1]), b_mul(ta, ab[2]));
+    ux = b_add(ux, ex);
+    uy = b_add(uy, ey);
+    uz = b_add(uz, ez);
+    return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
+}
+
 // One Boris momentum update on the scaled momentum u (steps a4-a9).
 // Returns 1/gamma^{n+1/2}; writes gamma^{n+1/2} to `gamma`.
 template <typename FP>
@@ -112,30 +162,14 @@ __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP E
     const FP inv_gn = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
     // a6: rotation vectors (eq. 13)
     const FP ta = b_mul(tc.alpha, inv_gn);
-    const FP tx = b_mul(ta, Bx), ty = b_mul(ta, By), tz = b_mul(ta, Bz);
-    const FP sf = b_mul(FP(2), b_rcpx(b_add(FP(1), b_norm2(tx, ty, tz))));
-    const FP sx = b_mul(sf, tx), sy = b_mul(sf, ty), sz = b_mul(sf, tz);
-    // a7: rotation (eq. 12): u' = u^- + u^- x t ; u^+ = u^- + u' x s
-    const FP upx = b_add(ux, b_cross(uy, tz, uz, ty));
-    const FP upy = b_add(uy, b_cross(uz, tx, ux, tz));
-    const FP upz = b_add(uz, b_cross(ux, ty, uy, tx));
-    ux = b_add(ux, b_cross(upy, sz, upz, sy));
-    uy = b_add(uy, b_cross(upz, sx, upx, sz));
-    uz = b_add(uz, b_cross(upx, sy, upy, sx));
+    // a6-a7: s and the rotation (eq. 12-13)
+    boris_rotate<FP>(ux, uy, uz, b_mul(ta, Bx), b_mul(ta, By), b_mul(ta, Bz));
     // a8: second electric half kick (eq. 10)
     ux = b_add(ux, ex);
     uy = b_add(uy, ey);
     uz = b_add(uz, ez);
     // a9: gamma^{n+1/2} (eq. 5, reading c3) and its reciprocal
-    const FP g2 = b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1));
-#ifdef BORIS_PRECISE_MATH
-    gamma = b_sqrt(g2);
-    return b_rcp(gamma);
-#else
-    const FP inv_g = b_rsqrt(g2);
-    gamma = b_mul(g2, inv_g);
-    return inv_g;
-#endif
+    return boris_gamma<FP>(ux, uy, uz, tc.kappa2, gamma);
 }
 
 // One full Boris step of one particle on stored quantities (rows a1-a11):

@@ -239,6 +239,17 @@ __global__ void __launch_bounds__(kFusedThreads)
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
         FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
         FP gam = FP(1);
+        // uniform / plane wave: E = c e, B = c b with fixed e, b -> per-particle aE e, alpha b
+        FP ae[3], ab[3];
+        if constexpr (FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE) {
+            const FP *ev = FIELD == FK_UNIFORM ? fa.E : fa.cE;
+            const FP *bv = FIELD == FK_UNIFORM ? fa.B : fa.cB;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                ae[k] = b_mul(tc.aE, ev[k]);
+                ab[k] = b_mul(tc.alpha, bv[k]);
+            }
+        }
         for (int64_t s0 = 0; s0 < n_steps; s0 += kFlush) {
             FP phia = FP(0);
             if constexpr (FIELD == FK_PLANE_WAVE)
@@ -247,17 +258,16 @@ __global__ void __launch_bounds__(kFusedThreads)
             FP dx = FP(0), dy = FP(0), dz = FP(0);
             const int m = (n_steps - s0) < kFlush ? (int)(n_steps - s0) : kFlush;
             for (int j = 0; j < m; ++j) {
-                FP Ex, Ey, Ez, Bx, By, Bz;
+                FP inv_g;
                 if constexpr (FIELD == FK_UNIFORM) {
-                    Ex = fa.E[0]; Ey = fa.E[1]; Ez = fa.E[2];
-                    Bx = fa.B[0]; By = fa.B[1]; Bz = fa.B[2];
+                    inv_g = boris_momentum_dir<FP, true>(ux, uy, uz, FP(1), ae, ab, tc.kappa2, gam);
                 } else if constexpr (FIELD == FK_PLANE_WAVE) {
                     const FP phi = b_fma(fa.kf[0], dx, b_fma(fa.kf[1], dy, b_fma(fa.kf[2], dz,
                                    b_fma(-(FP)j, fa.wdtf, phia))));
-                    const FP c = cos_small(phi);
-                    Ex = b_mul(fa.cE[0], c); Ey = b_mul(fa.cE[1], c); Ez = b_mul(fa.cE[2], c);
-                    Bx = b_mul(fa.cB[0], c); By = b_mul(fa.cB[1], c); Bz = b_mul(fa.cB[2], c);
+                    const FP c = cos_small(phi);  // E = E0 e_hat c, B = E0 (k_hat x e_hat) c
+                    inv_g = boris_momentum_dir<FP, false>(ux, uy, uz, c, ae, ab, tc.kappa2, gam);
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
+                    FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
                     const FP R = b_sqrt(b_norm2(x, y, z));
                     FP g1, g2, f3;
@@ -273,8 +283,8 @@ __global__ void __launch_bounds__(kFusedThreads)
                     Bx = b_mul(b_mul(sk, x), z);
                     By = b_mul(b_mul(sk, y), z);
                     Bz = b_mul(sb, b_fma(k2g2, b_mul(z, z), f3));
+                    inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 }
-                const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 // a10 (eq. 7): displacement accumulated in the window
                 const FP ct = b_mul(tc.cr, inv_g);
                 dx = b_fma(ct, ux, dx);
