@@ -119,7 +119,13 @@ class Workload:
         """
         if count is None:
             count = self.n - first
-        idx = torch.arange(first, first + count, dtype=torch.int64, device=device)
+        return self.generate_indices(
+            torch.arange(first, first + count, dtype=torch.int64, device=device))
+
+    def generate_indices(self, idx: torch.Tensor):
+        """The particles with the given global indices (int64 tensor), as generate()."""
+        device = idx.device
+        count = idx.numel()
         out = {}
         out["x"], out["y"], out["z"] = in_sphere(self.seed, idx, SPHERE_RADIUS)
         if self.mom_kind == "rest":

@@ -498,6 +498,47 @@ def _sampled_full_size(name, layout, precision, n_steps, n=None, sample=20_000):
     return er, ep
 
 
+def test_full_size_C5_bench_configuration():
+    """BASELINE configs[4] at its full single-GPU size (8e8, the bench's N=1 launch
+    configuration: streaming kernel + fused KE, one step): sampled trajectories vs the
+    oracle, and the device KE sum vs the oracle's Neumaier KE of the GPU's own state
+    (checks the full-size partial reduction)."""
+    import oracle as orc
+    w = synth.config("C5")
+    n = w.n
+    ens = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity)
+    chunk = 1 << 24
+    for c0 in range(0, n, chunk):
+        ens.fill(w.generate(c0, min(chunk, n - c0), device="cuda"), first=c0)
+    ens.wrap()
+    idx = np.unique(np.r_[np.linspace(0, n - 1, 20_000).astype(np.int64), n - 1])
+    ds = rounded(w.generate_indices(torch.from_numpy(idx)), "fp32")
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(ens.handle, ens.field, w.dt, 1, diag.data_ptr())
+    torch.cuda.synchronize()
+    assert diag[1].item() == n
+    ref = OracleRun(w, ds, "fp32")
+    ref.push(1)
+    it = torch.from_numpy(idx).cuda()
+    r = torch.stack([ens.t[k][it] for k in ("x", "y", "z")], 1).double().cpu().numpy()
+    p = torch.stack([ens.t[k][it] for k in ("px", "py", "pz")], 1).double().cpu().numpy()
+    metric = C15()
+    assert metric("r", r, ref.pos) <= TOL["fp32"]
+    assert metric("p", p, ref.mom) <= TOL["fp32"]
+    # KE of the GPU state, summed by the oracle on the host chunk by chunk (Neumaier)
+    parts = []
+    for c0 in range(0, n, chunk):
+        sl = slice(c0, min(n, c0 + chunk))
+        mom = torch.stack([ens.t[k][sl] for k in ("px", "py", "pz")], 1).double().cpu().numpy()
+        g = ens.t["gamma"][sl].double().cpu().numpy()
+        wgt = ens.t["weight"][sl].double().cpu().numpy()
+        parts.append(orc.kinetic_energy(mom, g, wgt, np.zeros(len(g), np.int16),
+                                        [w.types[0][1]], w.light_velocity))
+    ke_host = orc.neumaier_sum(parts)
+    assert diag[0].item() == pytest.approx(ke_host, rel=2e-6)
+    ens.close()
+
+
 def test_full_size_C2_fp32_soa_sampled():
     print(_sampled_full_size("C2", "soa", "fp32", 1))
 
