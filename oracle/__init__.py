@@ -14,6 +14,8 @@ Arrays are numpy, canonical double, xyz-interleaved (``pos``/``mom`` are
 * ``FIELD_UNIFORM``     params ``[Ex, Ey, Ez, Bx, By, Bz]``
 * ``FIELD_PLANE_WAVE``  params ``[E0, kx, ky, kz, ex, ey, ez, omega, k, phase0]``
 * ``FIELD_MDIPOLE``     params ``[A0, omega0, k, xi_star, n_terms]`` (eq. 14-15, readings c9-c13)
+* ``FIELD_GRID``        params ``[x0, y0, z0, dx, dy, dz, nx, ny, nz]``; ``E``/``B`` = node values
+  ``(3, nz, ny, nx)``, CIC gather on a periodic collocated grid (reading c-grid)
 
 Pins: ``tests/test_oracle_pins.py`` (closed forms, invariants, hand cases).
 """
@@ -29,6 +31,7 @@ FIELD_ARRAYS = 0
 FIELD_UNIFORM = 1
 FIELD_PLANE_WAVE = 2
 FIELD_MDIPOLE = 3
+FIELD_GRID = 4
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "boris_oracle.c")
@@ -65,6 +68,7 @@ def _load():
         lib.oracle_boris_step.restype = None
         lib.oracle_field_plane_wave.argtypes = [_dp, _dp, ctypes.c_double, _dp, _dp]
         lib.oracle_field_mdipole.argtypes = [_dp, _dp, ctypes.c_double, _dp, _dp]
+        lib.oracle_field_grid.argtypes = [_dp, _dp, _dp, _dp, _dp, _dp]
         lib.oracle_mdipole_radial.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                               _dp, _dp, _dp]
         lib.oracle_push.argtypes = [ctypes.c_int64, _dp, _dp, _dp, _i16p, _dp, _dp,
@@ -118,6 +122,11 @@ def push(pos, mom, type_, type_q, type_m, c, field_kind, params=None, E=None, B=
         Ea = _f64(E).reshape(n, 3)
         Ba = _f64(B).reshape(n, 3)
         pE, pB = _d(Ea), _d(Ba)
+    elif field_kind == FIELD_GRID:
+        # E, B: node values, component-major (3, nz, ny, nx) -> flat
+        Ea = _f64(E).reshape(-1)
+        Ba = _f64(B).reshape(-1)
+        pE, pB = _d(Ea), _d(Ba)
     else:
         pE = pB = ctypes.cast(None, _dp)
     rc = lib.oracle_push(n, _d(pos), _d(mom), _d(gamma), type_.ctypes.data_as(_i16p), _d(tq),
@@ -153,6 +162,17 @@ def field_plane_wave(params, r, t):
     E = np.zeros(3)
     B = np.zeros(3)
     lib.oracle_field_plane_wave(_d(_f64(params)), _d(_f64(r, (3,))), t, _d(E), _d(B))
+    return E, B
+
+
+def field_grid(params, gridE, gridB, r):
+    """CIC gather of node values (3, nz, ny, nx) at r (reading c-grid)."""
+    lib = _load()
+    E = np.zeros(3)
+    B = np.zeros(3)
+    gE = _f64(gridE).reshape(-1)
+    gB = _f64(gridB).reshape(-1)
+    lib.oracle_field_grid(_d(_f64(params)), _d(gE), _d(gB), _d(_f64(r, (3,))), _d(E), _d(B))
     return E, B
 
 

@@ -164,6 +164,45 @@ void oracle_field_mdipole(const double *params, const double r[3], double t,
     B[2] = sb * (k * k * g2 * z * z + f3);
 }
 
+/* Reading c-grid: CIC (cloud-in-cell, first-order) form factor on a periodic
+ * collocated grid.  Along each axis: xi = (x - x0)/dx, i0 = floor(xi), f = xi - i0,
+ * weights (1 - f, f) on nodes (i0 mod n, i0 + 1 mod n); the 3D weight of node
+ * (a, b, c) is the product of the three 1D weights. */
+static int64_t wrap_index(double i, int64_t n) {
+    double m = fmod(i, (double)n);
+    if (m < 0) m += (double)n;
+    return (int64_t)m;
+}
+
+void oracle_field_grid(const double *params, const double *gridE, const double *gridB,
+                       const double r[3], double E[3], double B[3]) {
+    int64_t n[3], idx[3][2];
+    double w[3][2];
+    int d, a, b, c;
+    for (d = 0; d < 3; ++d) {
+        n[d] = (int64_t)params[6 + d];
+        double xi = (r[d] - params[d]) / params[3 + d];
+        double i0 = floor(xi);
+        double f = xi - i0;
+        w[d][0] = 1.0 - f;
+        w[d][1] = f;
+        idx[d][0] = wrap_index(i0, n[d]);
+        idx[d][1] = wrap_index(i0 + 1.0, n[d]);
+    }
+    int64_t ncell = n[0] * n[1] * n[2];
+    for (d = 0; d < 3; ++d) E[d] = B[d] = 0.0;
+    for (c = 0; c < 2; ++c)
+        for (b = 0; b < 2; ++b)
+            for (a = 0; a < 2; ++a) {
+                int64_t node = (idx[2][c] * n[1] + idx[1][b]) * n[0] + idx[0][a];
+                double wt = w[0][a] * w[1][b] * w[2][c];
+                for (d = 0; d < 3; ++d) {
+                    E[d] += wt * gridE[d * ncell + node];
+                    B[d] += wt * gridB[d * ncell + node];
+                }
+            }
+}
+
 void oracle_field_at(int kind, const double *params, const double *fieldE,
                      const double *fieldB, int64_t i, const double r[3], double t,
                      double E[3], double B[3]) {
@@ -180,6 +219,9 @@ void oracle_field_at(int kind, const double *params, const double *fieldE,
         break;
     case ORACLE_FIELD_PLANE_WAVE:
         oracle_field_plane_wave(params, r, t, E, B);
+        break;
+    case ORACLE_FIELD_GRID:
+        oracle_field_grid(params, fieldE, fieldB, r, E, B);
         break;
     default:
         oracle_field_mdipole(params, r, t, E, B);

@@ -31,8 +31,20 @@ enum {
     ORACLE_FIELD_ARRAYS = 0,     /* per-particle E,B, constant over steps (L369-371, c6)   */
     ORACLE_FIELD_UNIFORM = 1,    /* params = {Ex,Ey,Ez,Bx,By,Bz}                            */
     ORACLE_FIELD_PLANE_WAVE = 2, /* params = {E0, kx,ky,kz (unit), ex,ey,ez (unit), omega, k, phase0} */
-    ORACLE_FIELD_MDIPOLE = 3     /* params = {A0, omega0, k, xi_star, n_terms}  eq.14-15, c9-c13 */
+    ORACLE_FIELD_MDIPOLE = 3,    /* params = {A0, omega0, k, xi_star, n_terms}  eq.14-15, c9-c13 */
+    ORACLE_FIELD_GRID = 4        /* params = {x0,y0,z0, dx,dy,dz, nx,ny,nz}; fieldE/fieldB =
+                                    Ex|Ey|Ez and Bx|By|Bz node values, 3*nx*ny*nz each
+                                    (component-major, node (i,j,k) at (k*ny+j)*nx+i);
+                                    reading c-grid, SURVEY §8(f) row 3 */
 };
+
+/* Field on a periodic collocated Cartesian grid gathered with CIC (trilinear)
+ * weights (reading c-grid; "each particle interacts with a
+ * set of nearby grid values of the electromagnetic field, depending on the form
+ * factor").  Node (i,j,k) sits at origin + (i dx, j dy, k dz); the grid repeats
+ * with period (nx dx, ny dy, nz dz). */
+void oracle_field_grid(const double *params, const double *gridE, const double *gridB,
+                       const double r[3], double E[3], double B[3]);
 
 /*
  * One Boris step of one particle, paper §2 (L147-186), p-form, double.

@@ -427,3 +427,82 @@ def test_openmp_driver_bitwise_equal_serial():
     b = oracle.push(*args, E=E, B=B, dt=0.05, n_steps=5, n_threads=4)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+# ---------------------------------------------------------------------------
+# Grid field gather (reading c-grid): CIC on a periodic grid.
+# ---------------------------------------------------------------------------
+
+GRID_P = [0.25, -1.0, 0.5, 0.5, 0.3, 0.7, 5, 7, 4]   # origin, spacing, (nx, ny, nz)
+
+
+def _grid_nodes(fn):
+    x0, y0, z0, dx, dy, dz, nx, ny, nz = GRID_P
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    X, Y, Z = x0 + i * dx, y0 + j * dy, z0 + k * dz
+    return np.stack([fn(X, Y, Z, c) for c in range(3)]), np.stack([fn(X, Y, Z, 3 + c)
+                                                                  for c in range(3)])
+
+
+def _multilinear(x, y, z, c):
+    a = [0.3, -1.1, 2.0, 0.7, -0.4, 1.3][c]
+    return a + 0.5 * x - 0.25 * y + 1.5 * z + 0.1 * x * y - 0.2 * y * z + 0.3 * x * z + 0.05 * x * y * z * (c + 1)
+
+
+def test_grid_gather_reproduces_multilinear_fields():
+    """CIC (trilinear) weights reproduce any multilinear function exactly inside the
+    grid (away from the periodic seam) -- pins the weights and the node indexing
+    (anisotropic grid: a swapped axis or stride fails)."""
+    gE, gB = _grid_nodes(_multilinear)
+    rng = np.random.default_rng(5)
+    x0, y0, z0, dx, dy, dz, nx, ny, nz = GRID_P
+    for _ in range(200):
+        r = np.array([x0 + rng.uniform(0, (nx - 1) * dx), y0 + rng.uniform(0, (ny - 1) * dy),
+                      z0 + rng.uniform(0, (nz - 1) * dz)])
+        E, B = oracle.field_grid(GRID_P, gE, gB, r)
+        ref = [_multilinear(r[0], r[1], r[2], c) for c in range(6)]
+        np.testing.assert_allclose(np.r_[E, B], ref, rtol=1e-13, atol=1e-13)
+
+
+def test_grid_gather_nodes_periodicity_partition_of_unity():
+    rng = np.random.default_rng(6)
+    x0, y0, z0, dx, dy, dz, nx, ny, nz = GRID_P
+    gE = rng.normal(size=(3, nz, ny, nx))
+    gB = rng.normal(size=(3, nz, ny, nx))
+    # exactly on a node: the node's values
+    i, j, k = 3, 5, 2
+    E, B = oracle.field_grid(GRID_P, gE, gB, [x0 + i * dx, y0 + j * dy, z0 + k * dz])
+    np.testing.assert_allclose(E, gE[:, k, j, i], rtol=1e-15, atol=1e-15)
+    np.testing.assert_allclose(B, gB[:, k, j, i], rtol=1e-15, atol=1e-15)
+    # periodic: shifting by a period along each axis (and negative coordinates)
+    r = np.array([0.9, -0.3, 1.1])
+    E0, B0 = oracle.field_grid(GRID_P, gE, gB, r)
+    for shift in ([nx * dx, 0, 0], [0, -ny * dy, 0], [0, 0, 3 * nz * dz]):
+        E1, B1 = oracle.field_grid(GRID_P, gE, gB, r + np.array(shift))
+        np.testing.assert_allclose(E1, E0, rtol=1e-12, atol=1e-13)
+        np.testing.assert_allclose(B1, B0, rtol=1e-12, atol=1e-13)
+    # across the seam: between the last node and node 0 the weights interpolate linearly
+    rs = np.array([x0 + (nx - 0.5) * dx, y0, z0])
+    E2, _ = oracle.field_grid(GRID_P, gE, gB, rs)
+    np.testing.assert_allclose(E2, 0.5 * (gE[:, 0, 0, nx - 1] + gE[:, 0, 0, 0]), rtol=1e-14)
+    # partition of unity: a constant grid is gathered as that constant
+    cE = np.broadcast_to(np.array([1.5, -2.0, 0.25])[:, None, None, None], (3, nz, ny, nx))
+    E3, _ = oracle.field_grid(GRID_P, cE, gB, rng.normal(size=3) * 10)
+    np.testing.assert_allclose(E3, [1.5, -2.0, 0.25], rtol=2e-15)
+
+
+def test_grid_push_with_constant_grid_equals_uniform_push():
+    """A constant grid field is the uniform field: trajectories agree to rounding."""
+    x0, y0, z0, dx, dy, dz, nx, ny, nz = GRID_P
+    E = np.array([0.0, 0.5, 0.1])
+    Bv = np.array([0.2, 0.0, 1.0])
+    gE = np.broadcast_to(E[:, None, None, None], (3, nz, ny, nx))
+    gB = np.broadcast_to(Bv[:, None, None, None], (3, nz, ny, nx))
+    rng = np.random.default_rng(8)
+    pos = rng.normal(size=(50, 3)) * 3
+    mom = rng.normal(size=(50, 3))
+    args = (pos, mom, np.zeros(50, np.int16), [-1.0], [1.0], 1.0)
+    P1, M1, _ = oracle.push(*args, oracle.FIELD_GRID, GRID_P, E=gE, B=gB, dt=0.1, n_steps=50)
+    P2, M2, _ = oracle.push(*args, oracle.FIELD_UNIFORM, np.r_[E, Bv], dt=0.1, n_steps=50)
+    np.testing.assert_allclose(M1, M2, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(P1, P2, rtol=1e-12, atol=1e-12)
