@@ -229,7 +229,37 @@ boris_status boris_field_create_plane_wave(double E0, const double k_hat[3],
  */
 boris_status boris_field_create_mdipole(double A0, double omega0, double k, boris_field **out);
 
+/*
+ * Grid field ("each particle interacts
+ * with a set of nearby grid values of the electromagnetic field, depending on the
+ * form factor"; reading c-grid): E, B given on the nodes of a periodic collocated
+ * Cartesian grid, node (i,j,k) at origin + (i, j, k) * spacing, gathered at each
+ * particle's position r^n every step with the CIC (trilinear) form factor.
+ * Ex..Bz: DEVICE arrays of nx*ny*nz FP on `device`, node (i,j,k) at
+ * (k*ny + j)*nx + i; they are copied (packed into 8-FP node records owned by
+ * the handle), so they may be freed after this call returns (synchronous).
+ * Errors: INVALID_ARG (n < 1, > 2^31 nodes, spacing <= 0, NULL), NO_DEVICE, CUDA.
+ * Ensembles pushed with it must have the same precision and device (MISMATCH).
+ */
+boris_status boris_field_create_grid(int32_t device, boris_precision precision, int32_t nx,
+                                     int32_t ny, int32_t nz, const double origin[3],
+                                     const double spacing[3], const void *Ex, const void *Ey,
+                                     const void *Ez, const void *Bx, const void *By,
+                                     const void *Bz, boris_field **out);
+
 boris_status boris_field_destroy(boris_field *field);
+
+/*
+ * Periodic particle sort ("we have to periodically sort the
+ * array of particles in order to improve cache locality"): reorder every array
+ * of `ens` (positions, momenta, weight, gamma, type; AoS records whole) by the
+ * grid cell of `grid` containing each particle.  Stable (particles of one cell
+ * keep their relative order), so the result is deterministic.  Per-particle
+ * field arrays are NOT permuted (they belong to the caller).  Device ensembles,
+ * n < 2^32.  Asynchronous (temporary buffers are stream-ordered allocations).
+ */
+boris_status boris_ensemble_sort_by_cell(boris_ensemble *ens, const boris_field *grid,
+                                         void *stream);
 
 /*
  * "Precalculated fields" (L369-371, reading c6): evaluate the analytic field

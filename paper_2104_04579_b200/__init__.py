@@ -49,6 +49,7 @@ EXPORTED = (
     "boris_ensemble_validate_types", "boris_ensemble_get_info", "boris_ensemble_get_time",
     "boris_ensemble_set_time", "boris_field_create_arrays_soa", "boris_field_create_arrays_aos",
     "boris_field_create_uniform", "boris_field_create_plane_wave", "boris_field_create_mdipole",
+    "boris_field_create_grid", "boris_ensemble_sort_by_cell",
     "boris_field_destroy", "boris_field_evaluate", "boris_push", "boris_push_diag", "boris_push_ex",
     "boris_kinetic_energy",
 )
@@ -94,6 +95,8 @@ _SIGNATURES = {
     "boris_field_create_plane_wave": ([_d, _dp, _dp, _d, _d, _d, _hp], _i32),
     "boris_field_create_mdipole": ([_d, _d, _d, _hp], _i32),
     "boris_field_destroy": ([_vp], _i32),
+    "boris_field_create_grid": ([_i32, _i32, _i32, _i32, _i32, _dp, _dp] + [_vp] * 6 + [_hp], _i32),
+    "boris_ensemble_sort_by_cell": ([_vp, _vp, _vp], _i32),
     "boris_field_evaluate": ([_vp, _vp, _d, _vp, _vp], _i32),
     "boris_push": ([_vp, _vp, _d, _i64, _vp], _i32),
     "boris_push_diag": ([_vp, _vp, _d, _i64, _vp, _vp], _i32),
@@ -310,6 +313,23 @@ def boris_field_create_mdipole(A0, omega0, k):
     _check(load_library().boris_field_create_mdipole(A0, omega0, k, ctypes.byref(h)),
            "boris_field_create_mdipole")
     return h.value
+
+
+def boris_field_create_grid(device, precision, nx, ny, nz, origin, spacing, Ex, Ey, Ez, Bx, By,
+                            Bz):
+    """Grid field (CIC gather); Ex..Bz are device pointers of nx*ny*nz FP (x fastest)."""
+    org = (ctypes.c_double * 3)(*[float(v) for v in origin])
+    sp = (ctypes.c_double * 3)(*[float(v) for v in spacing])
+    h = ctypes.c_void_p()
+    _check(load_library().boris_field_create_grid(device, precision, nx, ny, nz, org, sp, Ex, Ey,
+                                                  Ez, Bx, By, Bz, ctypes.byref(h)),
+           "boris_field_create_grid")
+    return h.value
+
+
+def boris_ensemble_sort_by_cell(ens, grid, stream=None):
+    _check(load_library().boris_ensemble_sort_by_cell(ens, grid, _stream(stream)),
+           "boris_ensemble_sort_by_cell")
 
 
 def boris_field_destroy(field):

@@ -132,6 +132,10 @@ struct boris_field {
     double E[3] = {0, 0, 0}, B[3] = {0, 0, 0};
     double E0 = 0, k_hat[3] = {0, 0, 0}, e_hat[3] = {0, 0, 0}, omega = 0, k = 0, phase0 = 0;
     double A0 = 0, omega0 = 0, kd = 0;
+    // grid (FK_GRID): owned packed node records on `device`, in `precision`
+    void *nodes = nullptr;
+    int gn[3] = {0, 0, 0};
+    double org[3] = {0, 0, 0}, h[3] = {0, 0, 0};
 };
 
 namespace {
@@ -268,6 +272,21 @@ Coefs<FP> make_coefs(const boris_ensemble *e, double dt) {
 }
 
 template <typename FP>
+GridArgs<FP> make_grid_args(const boris_field *f) {
+    GridArgs<FP> g;
+    memset(&g, 0, sizeof g);
+    g.nodes = (const FP *)f->nodes;
+    for (int d = 0; d < 3; ++d) {
+        g.org[d] = (FP)f->org[d];
+        g.inv_h[d] = (FP)(1.0 / f->h[d]);
+        g.nf[d] = (FP)f->gn[d];
+        g.inv_nf[d] = (FP)(1.0 / f->gn[d]);
+        g.n[d] = f->gn[d];
+    }
+    return g;
+}
+
+template <typename FP>
 AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
     AnalyticArgs<FP> a;
     memset(&a, 0, sizeof a);
@@ -298,6 +317,8 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
         a.mA02 = (FP)(-2.0 * f->A0);
         a.w0t0 = f->omega0 * t0;
         a.w0dt = f->omega0 * dt;
+    } else if (f->kind == FK_GRID) {
+        a.grid = make_grid_args<FP>(f);
     }
     return a;
 }
@@ -340,6 +361,9 @@ boris_status check_push_args(const boris_ensemble *e, const boris_field *f, doub
                         f->layout, f->precision, (long long)f->n, f->device, f->memory, e->layout,
                         e->precision, (long long)e->n, e->device, e->memory);
     }
+    if (f->kind == FK_GRID && (f->precision != e->precision || f->device != e->device))
+        return fail(BORIS_E_MISMATCH, "grid field (precision %d, device %d) does not match the "
+                    "ensemble (%d, %d)", f->precision, f->device, e->precision, e->device);
     return BORIS_OK;
 }
 
@@ -984,7 +1008,80 @@ boris_status boris_field_create_mdipole(double A0, double omega0, double k, bori
 }
 
 boris_status boris_field_destroy(boris_field *f) {
+    if (f && f->nodes) {
+        DeviceGuard g(f->device);
+        cudaFree(f->nodes);
+    }
     delete f;
+    return ok();
+}
+
+boris_status boris_field_create_grid(int32_t device, boris_precision precision, int32_t nx,
+                                     int32_t ny, int32_t nz, const double origin[3],
+                                     const double spacing[3], const void *Ex, const void *Ey,
+                                     const void *Ez, const void *Bx, const void *By,
+                                     const void *Bz, boris_field **out) {
+    if (!out || !origin || !spacing) return fail(BORIS_E_INVALID_ARG, "NULL argument");
+    if (precision != BORIS_FP32 && precision != BORIS_FP64)
+        return fail(BORIS_E_INVALID_ARG, "bad precision %d", precision);
+    if (nx < 1 || ny < 1 || nz < 1)
+        return fail(BORIS_E_INVALID_ARG, "grid dimensions must be >= 1");
+    const int64_t ncell = (int64_t)nx * ny * nz;
+    if (ncell > (int64_t)1 << 31) return fail(BORIS_E_INVALID_ARG, "grid larger than 2^31 nodes");
+    if (!finite3(origin) || !finite3(spacing) || !(spacing[0] > 0) || !(spacing[1] > 0) ||
+        !(spacing[2] > 0))
+        return fail(BORIS_E_INVALID_ARG, "origin must be finite and spacing > 0");
+    if (!Ex || !Ey || !Ez || !Bx || !By || !Bz)
+        return fail(BORIS_E_INVALID_ARG, "grid component arrays must be non-NULL");
+    boris_status s = check_device(device);
+    if (s != BORIS_OK) return s;
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    boris_field *f = new boris_field();
+    f->kind = FK_GRID;
+    f->precision = precision;
+    f->device = device;
+    f->gn[0] = nx;
+    f->gn[1] = ny;
+    f->gn[2] = nz;
+    for (int d = 0; d < 3; ++d) {
+        f->org[d] = origin[d];
+        f->h[d] = spacing[d];
+    }
+    cudaError_t err = cudaMalloc(&f->nodes, (size_t)ncell * 8 * fp_size(precision));
+    if (err != cudaSuccess) {
+        delete f;
+        return cuda_fail(err, "cudaMalloc(grid nodes)");
+    }
+    const void *comps[6] = {Ex, Ey, Ez, Bx, By, Bz};
+    err = launch_grid_pack(precision, ncell, comps, f->nodes, 0);
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) {
+        cudaFree(f->nodes);
+        delete f;
+        return cuda_fail(err, "grid packing");
+    }
+    *out = f;
+    return ok();
+}
+
+boris_status boris_ensemble_sort_by_cell(boris_ensemble *e, const boris_field *grid,
+                                         void *stream) {
+    if (!e || !grid) return fail(BORIS_E_INVALID_ARG, "NULL argument");
+    if (grid->kind != FK_GRID) return fail(BORIS_E_INVALID_ARG, "field is not a grid");
+    if (grid->precision != e->precision || grid->device != e->device)
+        return fail(BORIS_E_MISMATCH, "grid and ensemble differ in precision or device");
+    if (e->memory != BORIS_MEMORY_DEVICE)
+        return fail(BORIS_E_UNSUPPORTED, "sorting needs a device-resident ensemble");
+    if (e->n >= ((int64_t)1 << 32)) return fail(BORIS_E_UNSUPPORTED, "n >= 2^32");
+    DeviceGuard g(e->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    cudaError_t err = e->precision == BORIS_FP32
+                          ? sort_by_cell<float>(e->view(), make_grid_args<float>(grid), e->device,
+                                                (cudaStream_t)stream)
+                          : sort_by_cell<double>(e->view(), make_grid_args<double>(grid),
+                                                 e->device, (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "sort by cell");
     return ok();
 }
 
@@ -992,7 +1089,10 @@ boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensem
                                   const boris_field *out, void *stream) {
     if (!analytic || !e || !out) return fail(BORIS_E_INVALID_ARG, "NULL argument");
     if (analytic->kind == FK_ARRAYS)
-        return fail(BORIS_E_INVALID_ARG, "the source field must be analytic");
+        return fail(BORIS_E_INVALID_ARG, "the source field must be analytic or a grid");
+    if (analytic->kind == FK_GRID &&
+        (analytic->precision != e->precision || analytic->device != e->device))
+        return fail(BORIS_E_MISMATCH, "grid and ensemble differ in precision or device");
     if (!std::isfinite(t)) return fail(BORIS_E_INVALID_ARG, "t must be finite");
     if (out->kind != FK_ARRAYS || out->layout != e->layout || out->precision != e->precision ||
         out->n != e->n || out->device != e->device || out->memory != e->memory)

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "boris_device.cuh"
+#include "grid.cuh"
 #include "libboris.h"
 
 namespace boris {
@@ -15,7 +16,7 @@ constexpr int kAosThreads = 256;     // AoS tile kernel block size (one particle
 constexpr int kFusedThreads = 128;   // register-fused multi-step kernel block size
 constexpr int kFinalizeThreads = 1024;
 
-enum FieldKind { FK_ARRAYS = 0, FK_UNIFORM = 1, FK_PLANE_WAVE = 2, FK_MDIPOLE = 3 };
+enum FieldKind { FK_ARRAYS = 0, FK_UNIFORM = 1, FK_PLANE_WAVE = 2, FK_MDIPOLE = 3, FK_GRID = 4 };
 
 struct SoaPtrs {
     void *x, *y, *z, *px, *py, *pz, *w, *g;
@@ -45,6 +46,8 @@ struct AnalyticArgs {
     FP A0k2;         // 2 A0 k
     FP mA02;         // -2 A0
     double w0t0, w0dt;
+    // grid (FK_GRID): CIC gather of packed node records (grid.cuh)
+    GridArgs<FP> grid;
 };
 
 // Per-launch description of an ensemble's storage.
@@ -80,6 +83,14 @@ template <typename FP>
 cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
                          const Coefs<FP> &co, int64_t n_steps, bool multi, DiagOut *diag,
                          int device, cudaStream_t st);
+
+// Grid field support (k_grid.cu): pack 6 component arrays (ncell FP each) into
+// 8-FP node records; stable sort of an ensemble by grid cell (LSD radix sort of
+// (cell, index) pairs + permutation of every particle array).
+cudaError_t launch_grid_pack(int precision, int64_t ncell, const void *const comps[6],
+                             void *nodes, cudaStream_t st);
+template <typename FP>
+cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int device, cudaStream_t st);
 
 // Analytic field at every particle's position (time baked into fa) -> arrays.
 template <typename FP>

@@ -1,0 +1,95 @@
+// grid.cuh -- field gather from a periodic collocated Cartesian grid with the
+// CIC (cloud-in-cell, first-order) form factor (PAPER.md
+// L72-79, L89-91: "each particle interacts with a set of nearby grid values of
+// the electromagnetic field, depending on the form factor"; reading c-grid in
+// DESIGN.md).  Node (i,j,k) sits at origin + (i hx, j hy, k hz); the grid repeats
+// with period (nx hx, ny hy, nz hz).  Nodes are packed as 8-FP records
+// (Ex Ey Ez Bx | By Bz 0 0): two 128-bit loads per node in fp32, four in fp64.
+#pragma once
+
+#include "boris_device.cuh"
+
+namespace boris {
+
+template <typename FP>
+struct GridArgs {
+    const FP *nodes;  // 8 FP per node, node (i,j,k) at (k*ny + j)*nx + i
+    FP org[3];        // origin
+    FP inv_h[3];      // 1 / spacing
+    FP nf[3];         // n as FP
+    FP inv_nf[3];     // 1 / n
+    int n[3];
+};
+
+// One axis of the CIC weights: xi = (x - org)/h, base node floor(xi) wrapped into
+// [0, n), upper node base+1 (mod n), weight of the upper node f = xi - floor(xi).
+template <typename FP>
+__device__ __forceinline__ void grid_axis(FP x, FP org, FP inv_h, FP nf, FP inv_nf, int n,
+                                          int &i0, int &i1, FP &f) {
+    const FP xi = b_mul(b_add(x, -org), inv_h);
+    const FP fl = floor(xi);
+    f = b_add(xi, -fl);  // exact, in [0, 1)
+    const FP w = b_fma(-nf, floor(b_mul(fl, inv_nf)), fl);  // fl mod n, up to +-1 rounding
+    int i = (int)w;
+    if (i >= n) i -= n;
+    if (i < 0) i += n;
+    i0 = i;
+    i1 = (i + 1 == n) ? 0 : i + 1;
+}
+
+// Linear index of the cell whose base node is (i0, j0, k0): the sort key.
+template <typename FP>
+__device__ __forceinline__ uint32_t grid_cell(const GridArgs<FP> &g, FP x, FP y, FP z) {
+    int i0, i1, j0, j1, k0, k1;
+    FP f;
+    grid_axis<FP>(x, g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0], g.n[0], i0, i1, f);
+    grid_axis<FP>(y, g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1], g.n[1], j0, j1, f);
+    grid_axis<FP>(z, g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2], g.n[2], k0, k1, f);
+    return ((uint32_t)k0 * (uint32_t)g.n[1] + (uint32_t)j0) * (uint32_t)g.n[0] + (uint32_t)i0;
+}
+
+__device__ __forceinline__ void load_node(const float *nodes, uint32_t node, float (&e)[6]) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(nodes) + 2 * (size_t)node);
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(nodes) + 2 * (size_t)node + 1);
+    e[0] = a.x; e[1] = a.y; e[2] = a.z; e[3] = a.w; e[4] = b.x; e[5] = b.y;
+}
+__device__ __forceinline__ void load_node(const double *nodes, uint32_t node, double (&e)[6]) {
+    const double2 *p = reinterpret_cast<const double2 *>(nodes) + 4 * (size_t)node;
+    const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+    e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y; e[4] = c.x; e[5] = c.y;
+}
+
+// E, B at (x, y, z): sum over the 8 nodes of the cell of wx wy wz F_node.
+template <typename FP>
+__device__ __forceinline__ void grid_gather(const GridArgs<FP> &g, FP x, FP y, FP z, FP &Ex,
+                                            FP &Ey, FP &Ez, FP &Bx, FP &By, FP &Bz) {
+    int ix[2], iy[2], iz[2];
+    FP fx, fy, fz;
+    grid_axis<FP>(x, g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0], g.n[0], ix[0], ix[1], fx);
+    grid_axis<FP>(y, g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1], g.n[1], iy[0], iy[1], fy);
+    grid_axis<FP>(z, g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2], g.n[2], iz[0], iz[1], fz);
+    const FP wx[2] = {b_add(FP(1), -fx), fx};
+    const FP wy[2] = {b_add(FP(1), -fy), fy};
+    const FP wz[2] = {b_add(FP(1), -fz), fz};
+    FP acc[6] = {FP(0), FP(0), FP(0), FP(0), FP(0), FP(0)};
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const FP wyz = b_mul(wy[b], wz[c]);
+            const uint32_t row = ((uint32_t)iz[c] * (uint32_t)g.n[1] + (uint32_t)iy[b]) *
+                                 (uint32_t)g.n[0];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const FP wt = b_mul(wx[a], wyz);
+                FP node[6];
+                load_node(g.nodes, row + (uint32_t)ix[a], node);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = b_fma(wt, node[q], acc[q]);
+            }
+        }
+    Ex = acc[0]; Ey = acc[1]; Ez = acc[2];
+    Bx = acc[3]; By = acc[4]; Bz = acc[5];
+}
+
+}  // namespace boris

@@ -132,6 +132,8 @@ __device__ __forceinline__ void analytic_field(const AnalyticArgs<FP> &fa, doubl
         const FP c = cos_reduced(phi, FP(0));
         Ex = fa.cE[0] * c; Ey = fa.cE[1] * c; Ez = fa.cE[2] * c;
         Bx = fa.cB[0] * c; By = fa.cB[1] * c; Bz = fa.cB[2] * c;
+    } else if constexpr (FIELD == FK_GRID) {
+        grid_gather<FP>(fa.grid, (FP)rx, (FP)ry, (FP)rz, Ex, Ey, Ez, Bx, By, Bz);
     } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
         const FP x = (FP)rx, y = (FP)ry, z = (FP)rz;
         const FP R = sqrt(x * x + y * y + z * z);
@@ -266,6 +268,11 @@ __global__ void __launch_bounds__(kFusedThreads)
                                    b_fma(-(FP)j, fa.wdtf, phia))));
                     const FP c = cos_small(phi);  // E = E0 e_hat c, B = E0 (k_hat x e_hat) c
                     inv_g = boris_momentum_dir<FP, false>(ux, uy, uz, c, ae, ab, tc.kappa2, gam);
+                } else if constexpr (FIELD == FK_GRID) {  // CIC gather (reading c-grid)
+                    FP Ex, Ey, Ez, Bx, By, Bz;
+                    grid_gather<FP>(fa.grid, b_add((FP)xa, dx), b_add((FP)ya, dy),
+                                    b_add((FP)za, dz), Ex, Ey, Ez, Bx, By, Bz);
+                    inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
@@ -350,6 +357,9 @@ static cudaError_t dispatch_fused_field(const EnsView &e, int field_kind,
     case FK_MDIPOLE:
         return dispatch_fused_md<FP, LAYOUT, FK_MDIPOLE>(e, fa, co, n_steps, multi, diag, device,
                                                          st);
+    case FK_GRID:
+        return dispatch_fused_md<FP, LAYOUT, FK_GRID>(e, fa, co, n_steps, multi, diag, device,
+                                                      st);
     default:
         return cudaErrorInvalidValue;
     }
@@ -438,6 +448,9 @@ static cudaError_t dispatch_eval(const EnsView &e, int field_kind, const Analyti
         break;
     case FK_MDIPOLE:
         k_field_evaluate<FP, LAYOUT, FK_MDIPOLE><<<grid, kFusedThreads, 0, st>>>(e, fa, out, out_rec);
+        break;
+    case FK_GRID:
+        k_field_evaluate<FP, LAYOUT, FK_GRID><<<grid, kFusedThreads, 0, st>>>(e, fa, out, out_rec);
         break;
     default:
         return cudaErrorInvalidValue;

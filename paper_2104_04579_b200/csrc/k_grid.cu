@@ -1,0 +1,282 @@
+// k_grid.cu -- grid-field support: node packing and the
+// periodic particle sort by grid cell ("we have to periodically sort the array
+// of particles in order to improve cache locality").
+//
+// The sort is a stable LSD radix sort of (cell, original index) pairs written
+// here (8-bit digits, per-tile histograms, a recursive exclusive scan, and a
+// stable per-tile scatter using warp match_any ranks), followed by a gather of
+// every particle array through the sorted index.  Stable => particles of one
+// cell keep their relative order => the result is deterministic.
+#include <vector>
+
+#include "boris_internal.h"
+
+namespace boris {
+
+// ---------------------------------------------------------------------------
+// Node packing: comps[c][node] -> nodes[8*node + {0,1,2,3,4,5}], pads zeroed.
+// ---------------------------------------------------------------------------
+template <typename FP>
+__global__ void k_grid_pack(int64_t ncell, const FP *Ex, const FP *Ey, const FP *Ez,
+                            const FP *Bx, const FP *By, const FP *Bz, FP *nodes) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell; i += stride) {
+        FP *r = nodes + 8 * i;
+        r[0] = Ex[i]; r[1] = Ey[i]; r[2] = Ez[i];
+        r[3] = Bx[i]; r[4] = By[i]; r[5] = Bz[i];
+        r[6] = FP(0); r[7] = FP(0);
+    }
+}
+
+static unsigned grid1d(int64_t n, int threads = 256) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b > 65535 * 8) b = 65535 * 8;
+    return (unsigned)(b > 0 ? b : 1);
+}
+
+cudaError_t launch_grid_pack(int precision, int64_t ncell, const void *const c[6], void *nodes,
+                             cudaStream_t st) {
+    if (precision == BORIS_FP32)
+        k_grid_pack<float><<<grid1d(ncell), 256, 0, st>>>(
+            ncell, (const float *)c[0], (const float *)c[1], (const float *)c[2],
+            (const float *)c[3], (const float *)c[4], (const float *)c[5], (float *)nodes);
+    else
+        k_grid_pack<double><<<grid1d(ncell), 256, 0, st>>>(
+            ncell, (const double *)c[0], (const double *)c[1], (const double *)c[2],
+            (const double *)c[3], (const double *)c[4], (const double *)c[5], (double *)nodes);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Sort keys: the cell of each particle (grid_cell, the gather's own base node).
+// ---------------------------------------------------------------------------
+template <typename FP>
+__global__ void k_cell_keys(EnsView e, const __grid_constant__ GridArgs<FP> g, uint32_t *keys,
+                            uint32_t *vals) {
+    constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e.n; i += stride) {
+        FP x, y, z;
+        if (e.layout == BORIS_LAYOUT_SOA) {
+            x = ((const FP *)e.soa.x)[i];
+            y = ((const FP *)e.soa.y)[i];
+            z = ((const FP *)e.soa.z)[i];
+        } else {
+            const FP *r = (const FP *)((const unsigned char *)e.aos + i * RB);
+            x = r[0]; y = r[1]; z = r[2];
+        }
+        keys[i] = grid_cell<FP>(g, x, y, z);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// LSD radix sort, 8-bit digits.  Tile = 256 threads x 8 keys; in round r thread t
+// owns key tile0 + r*256 + t, so (round, thread) order is the original order.
+// ---------------------------------------------------------------------------
+constexpr int kRsThreads = 256;
+constexpr int kRsItems = 8;
+constexpr int kRsTile = kRsThreads * kRsItems;
+constexpr int kRsWarps = kRsThreads / 32;
+
+__global__ void __launch_bounds__(kRsThreads)
+    k_rs_hist(const uint32_t *keys, int64_t n, int shift, uint32_t *hist, int64_t nb) {
+    __shared__ uint32_t cnt[256];
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+#pragma unroll
+    for (int r = 0; r < kRsItems; ++r) {
+        const int64_t i = t0 + r * kRsThreads + threadIdx.x;
+        if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = cnt[threadIdx.x];  // digit-major
+}
+
+__global__ void __launch_bounds__(kRsThreads)
+    k_rs_scatter(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                 uint32_t *vals_out, int64_t n, int shift, const uint32_t *offs, int64_t nb) {
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t wcnt[kRsWarps][257];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    base[threadIdx.x] = offs[(int64_t)threadIdx.x * nb + blockIdx.x];
+    for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
+    if (threadIdx.x < kRsWarps) wcnt[threadIdx.x][256] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int r = 0; r < kRsItems; ++r) {
+        const int64_t i = t0 + r * kRsThreads + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t key = valid ? keys_in[i] : 0u;
+        const uint32_t val = valid ? vals_in[i] : 0u;
+        const int d = valid ? (int)((key >> shift) & 0xFFu) : 256;  // 256: no-op bin
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int rank = __popc(peers & lt);
+        if (rank == 0) wcnt[warp][d] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t before = 0;
+            for (int w = 0; w < warp; ++w) before += wcnt[w][d];
+            const uint32_t pos = base[d] + before + (uint32_t)rank;
+            keys_out[pos] = key;
+            vals_out[pos] = val;
+        }
+        __syncthreads();
+        uint32_t tot = 0;
+        for (int w = 0; w < kRsWarps; ++w) {
+            tot += wcnt[w][threadIdx.x];
+            wcnt[w][threadIdx.x] = 0;
+        }
+        base[threadIdx.x] += tot;
+        if (threadIdx.x < kRsWarps) wcnt[threadIdx.x][256] = 0;
+        __syncthreads();
+    }
+}
+
+// Exclusive scan of uint32 (64-bit running totals fit: n < 2^32 particles).
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanChunk = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_chunks(uint32_t *data, int64_t len, uint32_t *chunk_tot) {
+    __shared__ uint32_t s[kScanThreads];
+    const int64_t c0 = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = (c0 + k < len) ? data[c0 + k] : 0u;
+        sum += v[k];
+    }
+    s[threadIdx.x] = sum;
+    __syncthreads();
+    for (int off = 1; off < kScanThreads; off <<= 1) {  // Hillis-Steele inclusive
+        const uint32_t add = threadIdx.x >= (unsigned)off ? s[threadIdx.x - off] : 0u;
+        __syncthreads();
+        s[threadIdx.x] += add;
+        __syncthreads();
+    }
+    uint32_t run = s[threadIdx.x] - sum;  // exclusive prefix of this thread
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (c0 + k < len) data[c0 + k] = run;
+        run += v[k];
+    }
+    if (threadIdx.x == kScanThreads - 1 && chunk_tot) chunk_tot[blockIdx.x] = s[threadIdx.x];
+}
+
+__global__ void k_scan_add(uint32_t *data, int64_t len, const uint32_t *chunk_off) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < len) data[i] += chunk_off[i / kScanChunk];
+}
+
+static cudaError_t exclusive_scan(uint32_t *data, int64_t len, cudaStream_t st) {
+    const int64_t chunks = (len + kScanChunk - 1) / kScanChunk;
+    if (chunks <= 1) {
+        k_scan_chunks<<<1, kScanThreads, 0, st>>>(data, len, nullptr);
+        return cudaGetLastError();
+    }
+    uint32_t *tot = nullptr;
+    cudaError_t err = cudaMallocAsync((void **)&tot, (size_t)chunks * sizeof(uint32_t), st);
+    if (err != cudaSuccess) return err;
+    k_scan_chunks<<<(unsigned)chunks, kScanThreads, 0, st>>>(data, len, tot);
+    if ((err = exclusive_scan(tot, chunks, st)) == cudaSuccess) {
+        k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(data, len, tot);
+        err = cudaGetLastError();
+    }
+    cudaFreeAsync(tot, st);
+    return err;
+}
+
+// ---------------------------------------------------------------------------
+// Permutation: out[i] = in[perm[i]] for every particle array.
+// ---------------------------------------------------------------------------
+template <int BYTES>
+__global__ void k_gather_bytes(const unsigned char *in, unsigned char *out, const uint32_t *perm,
+                               int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t j = perm[i];
+        if constexpr (BYTES % 4 == 0) {
+            const uint32_t *s = (const uint32_t *)(in + j * BYTES);
+            uint32_t *d = (uint32_t *)(out + i * BYTES);
+#pragma unroll
+            for (int k = 0; k < BYTES / 4; ++k) d[k] = s[k];
+        } else {
+            const unsigned short *s = (const unsigned short *)(in + j * BYTES);
+            unsigned short *d = (unsigned short *)(out + i * BYTES);
+#pragma unroll
+            for (int k = 0; k < BYTES / 2; ++k) d[k] = s[k];
+        }
+    }
+}
+
+template <int BYTES>
+static cudaError_t permute_array(void *arr, void *tmp, const uint32_t *perm, int64_t n,
+                                 cudaStream_t st) {
+    k_gather_bytes<BYTES><<<grid1d(n), 256, 0, st>>>((const unsigned char *)arr,
+                                                     (unsigned char *)tmp, perm, n);
+    cudaError_t err = cudaGetLastError();
+    if (err == cudaSuccess)
+        err = cudaMemcpyAsync(arr, tmp, (size_t)n * BYTES, cudaMemcpyDeviceToDevice, st);
+    return err;
+}
+
+template <typename FP>
+cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/,
+                         cudaStream_t st) {
+    const int64_t n = e.n;
+    if (n <= 1) return cudaSuccess;
+    const uint64_t ncell = (uint64_t)g.n[0] * g.n[1] * g.n[2];
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < ncell) ++bits;
+    const int passes = (bits + 7) / 8;
+    const int64_t nb = (n + kRsTile - 1) / kRsTile;
+    constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
+    const size_t tmp_bytes = (size_t)n * (e.layout == BORIS_LAYOUT_SOA ? sizeof(FP) : RB);
+    unsigned char *buf = nullptr;
+    const size_t kv = (size_t)n * sizeof(uint32_t);
+    const size_t hist_bytes = (size_t)256 * nb * sizeof(uint32_t);
+    cudaError_t err = cudaMallocAsync((void **)&buf, 4 * kv + hist_bytes + tmp_bytes + 256, st);
+    if (err != cudaSuccess) return err;
+    uint32_t *k0 = (uint32_t *)buf, *v0 = k0 + n, *k1 = v0 + n, *v1 = k1 + n;
+    uint32_t *hist = v1 + n;
+    unsigned char *tmp = (unsigned char *)(hist + 256 * nb);
+    tmp = (unsigned char *)(((uintptr_t)tmp + 255) & ~(uintptr_t)255);
+
+    k_cell_keys<FP><<<grid1d(n), 256, 0, st>>>(e, g, k0, v0);
+    err = cudaGetLastError();
+    for (int p = 0; p < passes && err == cudaSuccess; ++p) {
+        k_rs_hist<<<(unsigned)nb, kRsThreads, 0, st>>>(k0, n, 8 * p, hist, nb);
+        if ((err = cudaGetLastError()) != cudaSuccess) break;
+        if ((err = exclusive_scan(hist, 256 * nb, st)) != cudaSuccess) break;
+        k_rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(k0, v0, k1, v1, n, 8 * p, hist, nb);
+        err = cudaGetLastError();
+        uint32_t *t;
+        t = k0; k0 = k1; k1 = t;
+        t = v0; v0 = v1; v1 = t;
+    }
+    // v0 = sorted original indices: apply to every particle array
+    if (err == cudaSuccess) {
+        if (e.layout == BORIS_LAYOUT_SOA) {
+            void *arrs[8] = {e.soa.x, e.soa.y, e.soa.z, e.soa.px, e.soa.py, e.soa.pz, e.soa.w, e.soa.g};
+            for (int a = 0; a < 8 && err == cudaSuccess; ++a)
+                if (arrs[a]) err = permute_array<sizeof(FP)>(arrs[a], tmp, v0, n, st);
+            if (err == cudaSuccess && e.soa.type)
+                err = permute_array<2>(e.soa.type, tmp, v0, n, st);
+        } else {
+            err = permute_array<RB>(e.aos, tmp, v0, n, st);
+        }
+    }
+    cudaFreeAsync(buf, st);
+    return err;
+}
+
+template cudaError_t sort_by_cell<float>(const EnsView &, const GridArgs<float> &, int,
+                                         cudaStream_t);
+template cudaError_t sort_by_cell<double>(const EnsView &, const GridArgs<double> &, int,
+                                          cudaStream_t);
+
+}  // namespace boris
