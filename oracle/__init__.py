@@ -81,6 +81,10 @@ def _load():
         lib.oracle_neumaier_sum.argtypes = [ctypes.c_int64, _dp]
         lib.oracle_neumaier_sum.restype = ctypes.c_double
         lib.oracle_max_threads.restype = ctypes.c_int
+        for name in ("oracle_vay_step", "oracle_hc_step"):
+            getattr(lib, name).argtypes = lib.oracle_boris_step.argtypes
+            getattr(lib, name).restype = None
+        lib.oracle_set_pusher.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -96,20 +100,29 @@ def _f64(a, shape=None):
     return a
 
 
-def boris_step(r, p, q, m, c, E, B, dt):
-    """One Boris step of one particle (L175-186).  Returns (r_new, p_new, gamma)."""
+PUSHER_BORIS = 0
+PUSHER_VAY = 1
+PUSHER_HIGUERA_CARY = 2
+
+
+def boris_step(r, p, q, m, c, E, B, dt, pusher=PUSHER_BORIS):
+    """One step of one particle (Boris: L175-186; Vay / Higuera-Cary: readings c-vay,
+    c-hc).  Returns (r_new, p_new, gamma)."""
     lib = _load()
     r = _f64(r, (3,)).copy()
     p = _f64(p, (3,)).copy()
     g = np.zeros(1)
-    lib.oracle_boris_step(_d(r), _d(p), _d(g), q, m, c, _d(_f64(E, (3,))), _d(_f64(B, (3,))), dt)
+    fn = {PUSHER_BORIS: lib.oracle_boris_step, PUSHER_VAY: lib.oracle_vay_step,
+          PUSHER_HIGUERA_CARY: lib.oracle_hc_step}[pusher]
+    fn(_d(r), _d(p), _d(g), q, m, c, _d(_f64(E, (3,))), _d(_f64(B, (3,))), dt)
     return r, p, float(g[0])
 
 
 def push(pos, mom, type_, type_q, type_m, c, field_kind, params=None, E=None, B=None,
-         t0=0.0, dt=1.0, n_steps=1, n_threads=1):
+         t0=0.0, dt=1.0, n_steps=1, n_threads=1, pusher=PUSHER_BORIS):
     """Push copies of ``pos``/``mom`` ``n_steps`` steps.  Returns (pos, mom, gamma)."""
     lib = _load()
+    lib.oracle_set_pusher(int(pusher))
     pos = _f64(pos).reshape(-1, 3).copy()
     mom = _f64(mom).reshape(-1, 3).copy()
     n = pos.shape[0]
@@ -132,6 +145,7 @@ def push(pos, mom, type_, type_q, type_m, c, field_kind, params=None, E=None, B=
     rc = lib.oracle_push(n, _d(pos), _d(mom), _d(gamma), type_.ctypes.data_as(_i16p), _d(tq),
                          _d(tm), len(tq), c, field_kind, _d(params_a), pE, pB, t0, dt,
                          int(n_steps), int(n_threads))
+    lib.oracle_set_pusher(PUSHER_BORIS)
     if rc != 0:
         raise ValueError("oracle_push: type index out of range")
     if n_steps == 0:

@@ -62,6 +62,76 @@ void oracle_boris_step(double r[3], double p[3], double *gamma, double q, double
     for (k = 0; k < 3; ++k) r[k] = r[k] + dt * p[k] / (g * m);
 }
 
+/* gamma_new of Vay (2008) / Higuera-Cary (2017): the positive root of
+ * gamma^4 - sigma gamma^2 - (tau^2 + ustar^2) = 0, sigma = gamma_v^2 - tau^2. */
+static double alt_gamma_new(const double v[3], const double tau[3]) {
+    double g2 = 1.0 + dot(v, v);
+    double tau2 = dot(tau, tau);
+    double us = dot(v, tau);
+    double sigma = g2 - tau2;
+    return sqrt((sigma + sqrt(sigma * sigma + 4.0 * (tau2 + us * us))) / 2.0);
+}
+
+/* x = s [v + (v.t) t + v x t], s = 1/(1 + t^2): the solution of x = v + x x t. */
+static void alt_implicit_rotation(const double v[3], const double t[3], double x[3]) {
+    double s = 1.0 / (1.0 + dot(t, t));
+    double vt = dot(v, t), vxt[3];
+    int k;
+    cross(v, t, vxt);
+    for (k = 0; k < 3; ++k) x[k] = s * (v[k] + vt * t[k] + vxt[k]);
+}
+
+void oracle_vay_step(double r[3], double p[3], double *gamma, double q, double m, double c,
+                     const double E[3], const double B[3], double dt) {
+    double u[3], tau[3], uxt[3], up[3], t[3], un[3];
+    double mc = m * c;
+    int k;
+    for (k = 0; k < 3; ++k) {
+        u[k] = p[k] / mc;
+        tau[k] = q * B[k] * dt / (2.0 * mc);
+    }
+    double g_old = sqrt(1.0 + dot(u, u));
+    double beta[3] = {u[0] / g_old, u[1] / g_old, u[2] / g_old};
+    cross(beta, tau, uxt);
+    for (k = 0; k < 3; ++k) up[k] = u[k] + q * E[k] * dt / mc + uxt[k];
+    double g_new = alt_gamma_new(up, tau);
+    for (k = 0; k < 3; ++k) t[k] = tau[k] / g_new;
+    alt_implicit_rotation(up, t, un);
+    double g = sqrt(1.0 + dot(un, un));
+    *gamma = g;
+    for (k = 0; k < 3; ++k) {
+        p[k] = un[k] * mc;
+        r[k] = r[k] + dt * c * un[k] / g;
+    }
+}
+
+void oracle_hc_step(double r[3], double p[3], double *gamma, double q, double m, double c,
+                    const double E[3], const double B[3], double dt) {
+    double um[3], tau[3], eps[3], t[3], ub[3], ubxt[3];
+    double mc = m * c;
+    int k;
+    for (k = 0; k < 3; ++k) {
+        eps[k] = q * E[k] * dt / (2.0 * mc);
+        um[k] = p[k] / mc + eps[k];
+        tau[k] = q * B[k] * dt / (2.0 * mc);
+    }
+    double g_new = alt_gamma_new(um, tau);
+    for (k = 0; k < 3; ++k) t[k] = tau[k] / g_new;
+    alt_implicit_rotation(um, t, ub);
+    cross(ub, t, ubxt);
+    double un[3];
+    for (k = 0; k < 3; ++k) un[k] = ub[k] + eps[k] + ubxt[k];
+    double g = sqrt(1.0 + dot(un, un));
+    *gamma = g;
+    for (k = 0; k < 3; ++k) {
+        p[k] = un[k] * mc;
+        r[k] = r[k] + dt * c * un[k] / g;
+    }
+}
+
+static int g_pusher = ORACLE_PUSHER_BORIS;
+void oracle_set_pusher(int pusher) { g_pusher = pusher; }
+
 void oracle_field_uniform(const double *params, double E[3], double B[3]) {
     int k;
     for (k = 0; k < 3; ++k) {
@@ -254,8 +324,15 @@ int oracle_push(int64_t n, double *pos, double *mom, double *gamma,
             double E[3], B[3];
             int j = type[i];
             oracle_field_at(field_kind, params, fieldE, fieldB, i, pos + 3 * i, t_n, E, B);
-            oracle_boris_step(pos + 3 * i, mom + 3 * i, gamma + i, type_q[j], type_m[j], c,
-                              E, B, dt);
+            if (g_pusher == ORACLE_PUSHER_VAY)
+                oracle_vay_step(pos + 3 * i, mom + 3 * i, gamma + i, type_q[j], type_m[j], c, E,
+                                B, dt);
+            else if (g_pusher == ORACLE_PUSHER_HIGUERA_CARY)
+                oracle_hc_step(pos + 3 * i, mom + 3 * i, gamma + i, type_q[j], type_m[j], c, E,
+                               B, dt);
+            else
+                oracle_boris_step(pos + 3 * i, mom + 3 * i, gamma + i, type_q[j], type_m[j], c,
+                                  E, B, dt);
         }
     }
     return 0;

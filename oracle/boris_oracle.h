@@ -59,6 +59,30 @@ void oracle_field_grid(const double *params, const double *gridE, const double *
 void oracle_boris_step(double r[3], double p[3], double *gamma, double q, double m,
                        double c, const double E[3], const double B[3], double dt);
 
+/* Pusher selector for oracle_push (PAPER.md L111-113,
+ * L137-140 cite alternative relativistic pushers (ref. [11]) without giving them;
+ * readings c-vay / c-hc in DESIGN.md follow their original papers). */
+enum { ORACLE_PUSHER_BORIS = 0, ORACLE_PUSHER_VAY = 1, ORACLE_PUSHER_HIGUERA_CARY = 2 };
+
+/* Vay (Phys. Plasmas 15, 056701, 2008), in u = p/(mc) (reading c-vay):
+ *   u' = u + (q dt/(mc)) E + (u/gamma(u)) x tau,        tau = q B dt/(2 m c)
+ *   sigma = gamma'^2 - tau^2, u* = u'.tau,
+ *   gamma_new = sqrt((sigma + sqrt(sigma^2 + 4 (tau^2 + u*^2)))/2),
+ *   t = tau/gamma_new, s = 1/(1+t^2),  u_new = s [u' + (u'.t) t + u' x t],
+ *   then gamma = gamma(u_new), r += dt c u_new / gamma (eq. 7). */
+void oracle_vay_step(double r[3], double p[3], double *gamma, double q, double m, double c,
+                     const double E[3], const double B[3], double dt);
+
+/* Higuera & Cary (Phys. Plasmas 24, 052104, 2017), in u = p/(mc) (reading c-hc):
+ *   u- = u + eps, eps = q E dt/(2 m c);  gamma_new from (u-, tau) as in Vay;
+ *   t = tau/gamma_new, s = 1/(1+t^2), ubar = s [u- + (u-.t) t + u- x t],
+ *   u_new = ubar + eps + ubar x t,  gamma = gamma(u_new), r += dt c u_new / gamma. */
+void oracle_hc_step(double r[3], double p[3], double *gamma, double q, double m, double c,
+                    const double E[3], const double B[3], double dt);
+
+/* Select the pusher used by oracle_push (default ORACLE_PUSHER_BORIS). */
+void oracle_set_pusher(int pusher);
+
 /* Uniform field: E, B constant (SURVEY §8(c) "Analytic fields"). */
 void oracle_field_uniform(const double *params, double E[3], double B[3]);
 

@@ -506,3 +506,72 @@ def test_grid_push_with_constant_grid_equals_uniform_push():
     P2, M2, _ = oracle.push(*args, oracle.FIELD_UNIFORM, np.r_[E, Bv], dt=0.1, n_steps=50)
     np.testing.assert_allclose(M1, M2, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(P1, P2, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# Alternative pushers (readings c-vay, c-hc): Vay (2008) and
+# Higuera-Cary (2017).  The paper only cites them (L111-113, L137-140), so they are
+# pinned by the physics their authors designed them for.
+# ---------------------------------------------------------------------------
+
+ALT = [oracle.PUSHER_VAY, oracle.PUSHER_HIGUERA_CARY]
+
+
+@pytest.mark.parametrize("pusher", ALT)
+def test_alt_pushers_equal_boris_without_magnetic_field(pusher):
+    rng = np.random.default_rng(21)
+    for _ in range(50):
+        r0, p0, E = rng.normal(size=3), rng.normal(size=3) * 2, rng.normal(size=3)
+        a = oracle.boris_step(r0, p0, -1.0, 1.0, 1.0, E, [0, 0, 0], 0.3)
+        b = oracle.boris_step(r0, p0, -1.0, 1.0, 1.0, E, [0, 0, 0], 0.3, pusher=pusher)
+        np.testing.assert_allclose(b[1], a[1], rtol=1e-14, atol=1e-15)
+        np.testing.assert_allclose(b[0], a[0], rtol=1e-14, atol=1e-15)
+
+
+@pytest.mark.parametrize("pusher", ALT)
+def test_alt_pushers_keep_the_force_free_drift(pusher):
+    """E perp B, |E| < |B|: a particle moving at the drift velocity v_d = c E x B/B^2
+    feels no force.  Vay and Higuera-Cary keep it exactly for ANY dt (their design
+    goal); Boris does not (its gamma_n is not the drift gamma) -- the test
+    discriminates."""
+    c, m, q = 1.0, 1.0, -1.0
+    E, B = [0.0, 0.9, 0.0], [0.0, 0.0, 1.0]
+    bd = 0.9
+    ud = np.array([bd / math.sqrt(1 - bd * bd), 0.0, 0.0])
+    dt = 2.0   # |q| B dt/(gamma m c) ~ 0.9 rad per step: far from the small-step regime
+    P, M, G = oracle.push([[0, 0, 0]], [ud * m * c], [0], [q], [m], c, oracle.FIELD_UNIFORM,
+                          E + B, dt=dt, n_steps=100, pusher=pusher)
+    assert np.abs(M[0] / (m * c) - ud).max() < 1e-12
+    np.testing.assert_allclose(P[0], [100 * dt * bd * c, 0, 0], rtol=1e-12, atol=1e-12)
+    Pb, Mb, _ = oracle.push([[0, 0, 0]], [ud * m * c], [0], [q], [m], c, oracle.FIELD_UNIFORM,
+                            E + B, dt=dt, n_steps=100)
+    assert np.abs(Mb[0] / (m * c) - ud).max() > 1e-2
+
+
+def test_higuera_cary_conserves_energy_in_pure_magnetic_field():
+    rng = np.random.default_rng(22)
+    n = 200
+    mom = rng.normal(size=(n, 3)) * 5
+    B = rng.normal(size=(n, 3)) * 3
+    P, M, G = oracle.push(np.zeros((n, 3)), mom, np.zeros(n, np.int16), [1.0], [1.0], 1.0,
+                          oracle.FIELD_ARRAYS, E=np.zeros((n, 3)), B=B, dt=0.7, n_steps=100,
+                          pusher=oracle.PUSHER_HIGUERA_CARY)
+    assert np.abs(np.linalg.norm(M, axis=1) / np.linalg.norm(mom, axis=1) - 1).max() < 1e-13
+
+
+@pytest.mark.parametrize("pusher", ALT)
+def test_alt_pushers_converge_second_order_to_the_same_trajectory(pusher):
+    """Random fixed E, B: every pusher approximates the same ODE (eq. 3-5) to O(dt^2),
+    so its distance to Boris shrinks 100x when dt shrinks 10x."""
+    rng = np.random.default_rng(23)
+    n = 64
+    pos, mom = rng.normal(size=(n, 3)), rng.normal(size=(n, 3))
+    E, B = rng.normal(size=(n, 3)) * 0.5, rng.normal(size=(n, 3))
+    diffs = []
+    for N in (100, 1000):
+        dt = 2.0 / N
+        args = (pos, mom, np.zeros(n, np.int16), [-1.0], [1.0], 1.0, oracle.FIELD_ARRAYS)
+        Pa, Ma, _ = oracle.push(*args, E=E, B=B, dt=dt, n_steps=N)
+        Pb, Mb, _ = oracle.push(*args, E=E, B=B, dt=dt, n_steps=N, pusher=pusher)
+        diffs.append(np.abs(Pb - Pa).max())
+    assert 60 < diffs[0] / diffs[1] < 160, diffs
