@@ -328,6 +328,21 @@ boris_status boris_push_diag(boris_ensemble *ens, const boris_field *field, doub
 #define BORIS_PUSH_STREAM_EACH_STEP 1u
 
 /*
+ * Momentum-update scheme, bits 4-5 of the flags (the paper
+ * cites alternative relativistic pushers, L111-113, L137-140, ref. [11], without
+ * giving them; readings c-vay / c-hc in DESIGN.md follow their original papers):
+ *   BORIS_PUSH_PUSHER_BORIS (default): the paper's conventional Boris (L141-186);
+ *   BORIS_PUSH_PUSHER_VAY: Vay, Phys. Plasmas 15, 056701 (2008);
+ *   BORIS_PUSH_PUSHER_HIGUERA_CARY: Higuera & Cary, Phys. Plasmas 24, 052104 (2017).
+ * Same state, half-kick/position conventions and field sampling as Boris.  The
+ * alternatives run in the register-fused kernels (single steps included).
+ */
+#define BORIS_PUSH_PUSHER_BORIS 0x00u
+#define BORIS_PUSH_PUSHER_VAY 0x10u
+#define BORIS_PUSH_PUSHER_HIGUERA_CARY 0x20u
+#define BORIS_PUSH_PUSHER_MASK 0x30u
+
+/*
  * boris_push / boris_push_diag with explicit flags (see above); d_diag may be
  * NULL (no diagnostic) or a DEVICE buffer of 2 doubles as in boris_push_diag.
  * Unknown flag bits: INVALID_ARG.

@@ -85,6 +85,9 @@ def _load():
             getattr(lib, name).argtypes = lib.oracle_boris_step.argtypes
             getattr(lib, name).restype = None
         lib.oracle_set_pusher.argtypes = [ctypes.c_int]
+        lib.oracle_deposit_current.argtypes = [ctypes.c_int64, _dp, _dp, _dp, _i16p, _dp, _dp,
+                                               ctypes.c_double, ctypes.c_double, _dp, _dp]
+        lib.oracle_deposit_current.restype = None
         _lib = lib
     return _lib
 
@@ -188,6 +191,24 @@ def field_grid(params, gridE, gridB, r):
     gB = _f64(gridB).reshape(-1)
     lib.oracle_field_grid(_d(_f64(params)), _d(gE), _d(gB), _d(_f64(r, (3,))), _d(E), _d(B))
     return E, B
+
+
+def deposit_current(pos, mom, weight, type_, type_q, type_m, c, dt, params):
+    """Direct CIC current deposition at the half-step position (reading c-dep).
+    pos/mom: state after the push.  Returns J as (3, nz, ny, nx)."""
+    lib = _load()
+    pos = _f64(pos).reshape(-1, 3)
+    n = pos.shape[0]
+    mom = _f64(mom).reshape(n, 3)
+    weight = _f64(weight).reshape(n)
+    type_ = np.ascontiguousarray(np.asarray(type_, dtype=np.int16).reshape(n))
+    p = _f64(params).reshape(-1)
+    nx, ny, nz = int(p[6]), int(p[7]), int(p[8])
+    J = np.zeros((3, nz, ny, nx))
+    lib.oracle_deposit_current(n, _d(pos), _d(mom), _d(weight), type_.ctypes.data_as(_i16p),
+                               _d(_f64(type_q).reshape(-1)), _d(_f64(type_m).reshape(-1)), c, dt,
+                               _d(p), _d(J))
+    return J
 
 
 def field_mdipole(params, r, t):

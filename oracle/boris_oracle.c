@@ -273,6 +273,45 @@ void oracle_field_grid(const double *params, const double *gridE, const double *
             }
 }
 
+/* Reading c-dep: direct CIC current deposition at the half-step position. */
+void oracle_deposit_current(int64_t n, const double *pos, const double *mom,
+                            const double *weight, const int16_t *type, const double *type_q,
+                            const double *type_m, double c, double dt, const double *params,
+                            double *J) {
+    int64_t nn[3], i, node;
+    int d, a, b, cc;
+    for (d = 0; d < 3; ++d) nn[d] = (int64_t)params[6 + d];
+    int64_t ncell = nn[0] * nn[1] * nn[2];
+    double vol = params[3] * params[4] * params[5];
+    for (i = 0; i < 3 * ncell; ++i) J[i] = 0.0;
+    for (i = 0; i < n; ++i) {
+        const double *p = mom + 3 * i;
+        double m = type_m[type[i]], q = type_q[type[i]];
+        double g = sqrt(1.0 + dot(p, p) / (m * c * m * c));
+        double v[3], rh[3], w[3][2];
+        int64_t idx[3][2];
+        for (d = 0; d < 3; ++d) {
+            v[d] = p[d] / (g * m);
+            rh[d] = pos[3 * i + d] - 0.5 * dt * v[d];
+            double xi = (rh[d] - params[d]) / params[3 + d];
+            double i0 = floor(xi);
+            double f = xi - i0;
+            w[d][0] = 1.0 - f;
+            w[d][1] = f;
+            idx[d][0] = wrap_index(i0, nn[d]);
+            idx[d][1] = wrap_index(i0 + 1.0, nn[d]);
+        }
+        double qw = q * weight[i] / vol;
+        for (cc = 0; cc < 2; ++cc)
+            for (b = 0; b < 2; ++b)
+                for (a = 0; a < 2; ++a) {
+                    node = (idx[2][cc] * nn[1] + idx[1][b]) * nn[0] + idx[0][a];
+                    double wt = w[0][a] * w[1][b] * w[2][cc];
+                    for (d = 0; d < 3; ++d) J[d * ncell + node] += qw * wt * v[d];
+                }
+    }
+}
+
 void oracle_field_at(int kind, const double *params, const double *fieldE,
                      const double *fieldB, int64_t i, const double r[3], double t,
                      double E[3], double B[3]) {

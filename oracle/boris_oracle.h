@@ -59,6 +59,20 @@ void oracle_field_grid(const double *params, const double *gridE, const double *
 void oracle_boris_step(double r[3], double p[3], double *gamma, double q, double m,
                        double c, const double E[3], const double B[3], double dt);
 
+/*
+ * Current deposition ("the step after the push"; PAPER.md
+ * L89-92: "The grid values of the current J are computed and added to Maxwell's
+ * equations"; reading c-dep): direct CIC deposition of every particle's current
+ * q w v^{n+1/2} at its half-step position r^{n+1/2} = r^{n+1} - (dt/2) v^{n+1/2}
+ * onto the nodes of the periodic collocated grid `params` (as ORACLE_FIELD_GRID),
+ * divided by the cell volume: J[d*ncell + node] += q w v_d S(r - r_node)/(hx hy hz).
+ * pos/mom are the state AFTER the push (r^{n+1}, p^{n+1/2}); J is zeroed first.
+ */
+void oracle_deposit_current(int64_t n, const double *pos, const double *mom,
+                            const double *weight, const int16_t *type, const double *type_q,
+                            const double *type_m, double c, double dt, const double *params,
+                            double *J);
+
 /* Pusher selector for oracle_push (PAPER.md L111-113,
  * L137-140 cite alternative relativistic pushers (ref. [11]) without giving them;
  * readings c-vay / c-hc in DESIGN.md follow their original papers). */

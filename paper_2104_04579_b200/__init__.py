@@ -38,6 +38,10 @@ BORIS_MEMORY_HOST = 1
 BORIS_MAX_TYPES = 32
 BORIS_PUSH_AUTO = 0
 BORIS_PUSH_STREAM_EACH_STEP = 1
+BORIS_PUSH_PUSHER_BORIS = 0x00
+BORIS_PUSH_PUSHER_VAY = 0x10
+BORIS_PUSH_PUSHER_HIGUERA_CARY = 0x20
+BORIS_PUSH_PUSHER_MASK = 0x30
 BORIS_AOS_RECORD_BYTES = {BORIS_FP32: 36, BORIS_FP64: 72}
 BORIS_AOS_FIELD_BYTES = {BORIS_FP32: 24, BORIS_FP64: 48}
 

@@ -263,6 +263,7 @@ Coefs<FP> make_coefs(const boris_ensemble *e, double dt) {
         co.t[i].aE = (FP)(S * q * dt / 2.0);          // eq. 9-10
         co.t[i].alpha = (FP)(q * dt / (2.0 * mc));    // eq. 13
         co.t[i].kappa2 = (FP)(kappa * kappa);         // eq. 5
+        co.t[i].kappa = (FP)kappa;
         co.t[i].cr = (FP)(dt / (S * m));              // eq. 7
         co.t[i].S = (FP)S;
         co.t[i].invS = (FP)(1.0 / S);
@@ -329,21 +330,28 @@ cudaError_t push_view(const boris_ensemble *e, const EnsView &v, const boris_fie
                       const FieldSoaPtrs &fs, const void *faos, double t0, double dt,
                       int64_t n_steps, uint32_t flags, DiagOut *diag, cudaStream_t st) {
     const Coefs<FP> co = make_coefs<FP>(e, dt);
+    const int pusher = (int)((flags & BORIS_PUSH_PUSHER_MASK) >> 4);
     if (f->kind == FK_ARRAYS) {
-        if (n_steps > 1 && !(flags & BORIS_PUSH_STREAM_EACH_STEP))
-            return launch_fused_arrays<FP>(v, fs, faos, co, n_steps, e->multi(), diag, e->device,
-                                           st);
+        const bool each = (flags & BORIS_PUSH_STREAM_EACH_STEP) != 0;
+        if (n_steps > 1 && !each)
+            return launch_fused_arrays<FP>(v, fs, faos, co, n_steps, e->multi(), pusher, diag,
+                                           e->device, st);
         for (int64_t s = 0; s < n_steps; ++s) {
             DiagOut *d = (s == n_steps - 1) ? diag : nullptr;
-            cudaError_t err = v.layout == BORIS_LAYOUT_SOA
-                                  ? launch_stream_soa<FP>(v, fs, co, e->multi(), d, e->device, st)
-                                  : launch_stream_aos<FP>(v, faos, co, e->multi(), d, e->device, st);
+            cudaError_t err;
+            if (pusher != PUSHER_BORIS)  // streaming kernels are Boris-only: 1-step fused launch
+                err = launch_fused_arrays<FP>(v, fs, faos, co, 1, e->multi(), pusher, d,
+                                              e->device, st);
+            else
+                err = v.layout == BORIS_LAYOUT_SOA
+                          ? launch_stream_soa<FP>(v, fs, co, e->multi(), d, e->device, st)
+                          : launch_stream_aos<FP>(v, faos, co, e->multi(), d, e->device, st);
             if (err != cudaSuccess) return err;
         }
         return cudaSuccess;
     }
     const AnalyticArgs<FP> fa = make_analytic<FP>(f, t0, dt);
-    return launch_fused<FP>(v, f->kind, fa, co, n_steps, e->multi(), diag, e->device, st);
+    return launch_fused<FP>(v, f->kind, fa, co, n_steps, e->multi(), pusher, diag, e->device, st);
 }
 
 boris_status check_push_args(const boris_ensemble *e, const boris_field *f, double dt,
@@ -1120,7 +1128,8 @@ static boris_status push_impl(boris_ensemble *e, const boris_field *f, double dt
                               uint32_t flags, double *d_diag, cudaStream_t st) {
     boris_status s = check_push_args(e, f, dt, n_steps);
     if (s != BORIS_OK) return s;
-    if (flags & ~(uint32_t)BORIS_PUSH_STREAM_EACH_STEP)
+    if ((flags & ~(uint32_t)(BORIS_PUSH_STREAM_EACH_STEP | BORIS_PUSH_PUSHER_MASK)) ||
+        (flags & BORIS_PUSH_PUSHER_MASK) == BORIS_PUSH_PUSHER_MASK)
         return fail(BORIS_E_INVALID_ARG, "unknown push flags 0x%x", flags);
     if (n_steps == 0 && !d_diag) return ok();
     DeviceGuard g(e->device);

@@ -39,7 +39,11 @@ struct TypeCoef {
     FP S;       // 2^k              u = S p (exact)
     FP invS;    // 2^-k             p = invS u (exact)
     FP ke;      // m c^2 kappa^2 = 1/(S^2 m): KE = w ke |u|^2/(gamma+1)
+    FP kappa;   // 1 / (S m c)      (alternative pushers: u*.tau in true units)
 };
+
+// Momentum update scheme (readings c-vay, c-hc in DESIGN.md).
+enum Pusher { PUSHER_BORIS = 0, PUSHER_VAY = 1, PUSHER_HIGUERA_CARY = 2 };
 
 template <typename FP>
 struct Coefs {
@@ -172,17 +176,103 @@ __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP E
     return boris_gamma<FP>(ux, uy, uz, tc.kappa2, gamma);
 }
 
+// ---------------------------------------------------------------------------
+// Alternative pushers (Vay 2008; Higuera & Cary 2017), same scaled-u units:
+// u = S p, u_true = kappa u, tau = alpha B = q B dt/(2mc) (dimensionless).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float b_sqrtx(float x) {
+#ifdef BORIS_PRECISE_MATH
+    return __fsqrt_rn(x);
+#else
+    return b_mul(x, b_rsqrt(x));  // x > 0 here
+#endif
+}
+__device__ __forceinline__ double b_sqrtx(double x) { return __dsqrt_rn(x); }
+
+// gamma_new: positive root of g^4 - sigma g^2 - (tau^2 + u*^2) = 0 with
+// sigma = 1 + |v_true|^2 - tau^2 and u* = v_true . tau.
+template <typename FP>
+__device__ __forceinline__ FP alt_gamma(FP vx, FP vy, FP vz, FP tx, FP ty, FP tz, FP tau2,
+                                        const TypeCoef<FP> &tc) {
+    const FP sigma = b_add(b_fma(tc.kappa2, b_norm2(vx, vy, vz), FP(1)), -tau2);
+    const FP us = b_mul(tc.kappa, b_fma(vx, tx, b_fma(vy, ty, b_mul(vz, tz))));
+    const FP disc = b_fma(sigma, sigma, b_mul(FP(4), b_fma(us, us, tau2)));
+    return b_sqrtx(b_mul(FP(0.5), b_add(sigma, b_sqrtx(disc))));
+}
+
+// x = s [v + (v.t) t + v x t], s = 1/(1+t^2): the solution of x = v + x x t.
+template <typename FP>
+__device__ __forceinline__ void alt_rotate(FP vx, FP vy, FP vz, FP tx, FP ty, FP tz, FP &x,
+                                           FP &y, FP &z) {
+    const FP s = b_rcpx(b_add(FP(1), b_norm2(tx, ty, tz)));
+    const FP vt = b_fma(vx, tx, b_fma(vy, ty, b_mul(vz, tz)));
+    x = b_mul(s, b_add(b_fma(vt, tx, vx), b_cross(vy, tz, vz, ty)));
+    y = b_mul(s, b_add(b_fma(vt, ty, vy), b_cross(vz, tx, vx, tz)));
+    z = b_mul(s, b_add(b_fma(vt, tz, vz), b_cross(vx, ty, vy, tx)));
+}
+
+// Higuera-Cary: u- = u + eps; gamma_new(u-, tau); t = tau/gamma_new;
+// ubar = implicit rotation of u-; u = ubar + eps + ubar x t.
+template <typename FP>
+__device__ __forceinline__ FP hc_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP Ey, FP Ez, FP Bx,
+                                          FP By, FP Bz, const TypeCoef<FP> &tc, FP &gamma) {
+    const FP ex = b_mul(tc.aE, Ex), ey = b_mul(tc.aE, Ey), ez = b_mul(tc.aE, Ez);
+    ux = b_add(ux, ex);
+    uy = b_add(uy, ey);
+    uz = b_add(uz, ez);
+    const FP tx = b_mul(tc.alpha, Bx), ty = b_mul(tc.alpha, By), tz = b_mul(tc.alpha, Bz);
+    const FP tau2 = b_norm2(tx, ty, tz);
+    const FP ig = b_rcpx(alt_gamma<FP>(ux, uy, uz, tx, ty, tz, tau2, tc));
+    const FP sx = b_mul(tx, ig), sy = b_mul(ty, ig), sz = b_mul(tz, ig);
+    FP bx, by, bz;
+    alt_rotate<FP>(ux, uy, uz, sx, sy, sz, bx, by, bz);
+    ux = b_add(b_add(bx, ex), b_cross(by, sz, bz, sy));
+    uy = b_add(b_add(by, ey), b_cross(bz, sx, bx, sz));
+    uz = b_add(b_add(bz, ez), b_cross(bx, sy, by, sx));
+    return boris_gamma<FP>(ux, uy, uz, tc.kappa2, gamma);
+}
+
+// Vay: u' = u + 2 eps + (u/gamma(u)) x tau; gamma_new(u', tau); t = tau/gamma_new;
+// u = implicit rotation of u'.
+template <typename FP>
+__device__ __forceinline__ FP vay_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP Ey, FP Ez, FP Bx,
+                                           FP By, FP Bz, const TypeCoef<FP> &tc, FP &gamma) {
+    const FP ig0 = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
+    const FP tx = b_mul(tc.alpha, Bx), ty = b_mul(tc.alpha, By), tz = b_mul(tc.alpha, Bz);
+    const FP wx = b_mul(ux, ig0), wy = b_mul(uy, ig0), wz = b_mul(uz, ig0);
+    const FP a2 = b_mul(FP(2), tc.aE);
+    const FP px = b_add(b_fma(a2, Ex, ux), b_cross(wy, tz, wz, ty));
+    const FP py = b_add(b_fma(a2, Ey, uy), b_cross(wz, tx, wx, tz));
+    const FP pz = b_add(b_fma(a2, Ez, uz), b_cross(wx, ty, wy, tx));
+    const FP tau2 = b_norm2(tx, ty, tz);
+    const FP ig = b_rcpx(alt_gamma<FP>(px, py, pz, tx, ty, tz, tau2, tc));
+    alt_rotate<FP>(px, py, pz, b_mul(tx, ig), b_mul(ty, ig), b_mul(tz, ig), ux, uy, uz);
+    return boris_gamma<FP>(ux, uy, uz, tc.kappa2, gamma);
+}
+
+// Steps a4-a9 with the selected scheme.
+template <typename FP, int PUSHER>
+__device__ __forceinline__ FP momentum_update(FP &ux, FP &uy, FP &uz, FP Ex, FP Ey, FP Ez, FP Bx,
+                                              FP By, FP Bz, const TypeCoef<FP> &tc, FP &gamma) {
+    if constexpr (PUSHER == PUSHER_VAY)
+        return vay_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gamma);
+    else if constexpr (PUSHER == PUSHER_HIGUERA_CARY)
+        return hc_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gamma);
+    else
+        return boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gamma);
+}
+
 // One full Boris step of one particle on stored quantities (rows a1-a11):
 // p -> u (exact), boris_momentum, position update, u -> p (exact).  Shared by
 // every streaming path so they are bitwise identical.
-template <typename FP>
+template <typename FP, int PUSHER = PUSHER_BORIS>
 __device__ __forceinline__ void push_one(FP &x, FP &y, FP &z, FP &px, FP &py, FP &pz, FP &g,
                                          FP Ex, FP Ey, FP Ez, FP Bx, FP By, FP Bz,
                                          const TypeCoef<FP> &tc, FP &ux, FP &uy, FP &uz) {
     ux = b_mul(px, tc.S);
     uy = b_mul(py, tc.S);
     uz = b_mul(pz, tc.S);
-    const FP inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, g);
+    const FP inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, g);
     // a10: r^{n+1} = r^n + dt p^{n+1/2}/(gamma m) = r^n + (cr/gamma) u   (eq. 7)
     const FP ct = b_mul(tc.cr, inv_g);
     x = b_fma(ct, ux, x);

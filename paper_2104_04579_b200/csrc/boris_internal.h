@@ -81,8 +81,8 @@ cudaError_t launch_stream_aos(const EnsView &e, const void *field_records, const
 
 template <typename FP>
 cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
-                         const Coefs<FP> &co, int64_t n_steps, bool multi, DiagOut *diag,
-                         int device, cudaStream_t st);
+                         const Coefs<FP> &co, int64_t n_steps, bool multi, int pusher,
+                         DiagOut *diag, int device, cudaStream_t st);
 
 // Grid field support (k_grid.cu): pack 6 component arrays (ncell FP each) into
 // 8-FP node records; stable sort of an ensemble by grid cell (LSD radix sort of
@@ -102,7 +102,7 @@ cudaError_t launch_field_evaluate(const EnsView &e, int field_kind, const Analyt
 // n_steps launches of the streaming kernels.
 template <typename FP>
 cudaError_t launch_fused_arrays(const EnsView &e, const FieldSoaPtrs &f, const void *frec,
-                                const Coefs<FP> &co, int64_t n_steps, bool multi,
+                                const Coefs<FP> &co, int64_t n_steps, bool multi, int pusher,
                                 DiagOut *diag, int device, cudaStream_t st);
 
 template <typename FP>

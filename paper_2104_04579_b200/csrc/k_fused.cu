@@ -213,7 +213,7 @@ constexpr int kFlush = 8;
 // Launches are split into chunks of kTimeTab steps on the host.
 constexpr int kTimeTab = 1024;
 
-template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG>
+template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER>
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
@@ -262,17 +262,28 @@ __global__ void __launch_bounds__(kFusedThreads)
             for (int j = 0; j < m; ++j) {
                 FP inv_g;
                 if constexpr (FIELD == FK_UNIFORM) {
-                    inv_g = boris_momentum_dir<FP, true>(ux, uy, uz, FP(1), ae, ab, tc.kappa2, gam);
+                    if constexpr (PUSHER == PUSHER_BORIS)
+                        inv_g = boris_momentum_dir<FP, true>(ux, uy, uz, FP(1), ae, ab, tc.kappa2,
+                                                             gam);
+                    else
+                        inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, fa.E[0], fa.E[1], fa.E[2],
+                                                            fa.B[0], fa.B[1], fa.B[2], tc, gam);
                 } else if constexpr (FIELD == FK_PLANE_WAVE) {
                     const FP phi = b_fma(fa.kf[0], dx, b_fma(fa.kf[1], dy, b_fma(fa.kf[2], dz,
                                    b_fma(-(FP)j, fa.wdtf, phia))));
                     const FP c = cos_small(phi);  // E = E0 e_hat c, B = E0 (k_hat x e_hat) c
-                    inv_g = boris_momentum_dir<FP, false>(ux, uy, uz, c, ae, ab, tc.kappa2, gam);
+                    if constexpr (PUSHER == PUSHER_BORIS)
+                        inv_g = boris_momentum_dir<FP, false>(ux, uy, uz, c, ae, ab, tc.kappa2,
+                                                              gam);
+                    else
+                        inv_g = momentum_update<FP, PUSHER>(
+                            ux, uy, uz, b_mul(fa.cE[0], c), b_mul(fa.cE[1], c), b_mul(fa.cE[2], c),
+                            b_mul(fa.cB[0], c), b_mul(fa.cB[1], c), b_mul(fa.cB[2], c), tc, gam);
                 } else if constexpr (FIELD == FK_GRID) {  // CIC gather (reading c-grid)
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     grid_gather<FP>(fa.grid, b_add((FP)xa, dx), b_add((FP)ya, dy),
                                     b_add((FP)za, dz), Ex, Ey, Ez, Bx, By, Bz);
-                    inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
+                    inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                     Bx = b_mul(b_mul(sk, x), z);
                     By = b_mul(b_mul(sk, y), z);
                     Bz = b_mul(sb, b_fma(k2g2, b_mul(z, z), f3));
-                    inv_g = boris_momentum<FP>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
+                    inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 }
                 // a10 (eq. 7): displacement accumulated in the window
                 const FP ct = b_mul(tc.cr, inv_g);
@@ -314,61 +325,80 @@ __global__ void __launch_bounds__(kFusedThreads)
     if (DIAG) block_diag_partial<kFusedThreads>(ke, cnt, partials);
 }
 
-template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG>
+template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER>
 static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
                                   const Coefs<FP> &co, int64_t n_steps, DiagOut *diag,
                                   int device, cudaStream_t st) {
     const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    k_fused<FP, LAYOUT, FIELD, MULTI, DIAG><<<(unsigned)grid, kFusedThreads, 0, st>>>(
+    k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER><<<(unsigned)grid, kFusedThreads, 0, st>>>(
         e, fa, co, n_steps, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }
 
-template <typename FP, int LAYOUT, int FIELD>
+template <typename FP, int LAYOUT, int FIELD, int PUSHER>
 static cudaError_t dispatch_fused_md(const EnsView &e, const AnalyticArgs<FP> &fa,
                                      const Coefs<FP> &co, int64_t n_steps, bool multi,
                                      DiagOut *diag, int device, cudaStream_t st) {
     if (multi)
-        return diag ? dispatch_fused<FP, LAYOUT, FIELD, true, true>(e, fa, co, n_steps, diag,
-                                                                     device, st)
-                    : dispatch_fused<FP, LAYOUT, FIELD, true, false>(e, fa, co, n_steps, diag,
-                                                                      device, st);
-    return diag ? dispatch_fused<FP, LAYOUT, FIELD, false, true>(e, fa, co, n_steps, diag,
-                                                                  device, st)
-                : dispatch_fused<FP, LAYOUT, FIELD, false, false>(e, fa, co, n_steps, diag,
-                                                                   device, st);
+        return diag ? dispatch_fused<FP, LAYOUT, FIELD, true, true, PUSHER>(e, fa, co, n_steps,
+                                                                             diag, device, st)
+                    : dispatch_fused<FP, LAYOUT, FIELD, true, false, PUSHER>(e, fa, co, n_steps,
+                                                                              diag, device, st);
+    return diag ? dispatch_fused<FP, LAYOUT, FIELD, false, true, PUSHER>(e, fa, co, n_steps, diag,
+                                                                          device, st)
+                : dispatch_fused<FP, LAYOUT, FIELD, false, false, PUSHER>(e, fa, co, n_steps,
+                                                                           diag, device, st);
 }
 
-template <typename FP, int LAYOUT>
+template <typename FP, int LAYOUT, int PUSHER>
 static cudaError_t dispatch_fused_field(const EnsView &e, int field_kind,
                                         const AnalyticArgs<FP> &fa, const Coefs<FP> &co,
                                         int64_t n_steps, bool multi, DiagOut *diag, int device,
                                         cudaStream_t st) {
     switch (field_kind) {
     case FK_UNIFORM:
-        return dispatch_fused_md<FP, LAYOUT, FK_UNIFORM>(e, fa, co, n_steps, multi, diag, device,
-                                                         st);
+        return dispatch_fused_md<FP, LAYOUT, FK_UNIFORM, PUSHER>(e, fa, co, n_steps, multi, diag,
+                                                                 device, st);
     case FK_PLANE_WAVE:
-        return dispatch_fused_md<FP, LAYOUT, FK_PLANE_WAVE>(e, fa, co, n_steps, multi, diag,
-                                                            device, st);
+        return dispatch_fused_md<FP, LAYOUT, FK_PLANE_WAVE, PUSHER>(e, fa, co, n_steps, multi,
+                                                                    diag, device, st);
     case FK_MDIPOLE:
-        return dispatch_fused_md<FP, LAYOUT, FK_MDIPOLE>(e, fa, co, n_steps, multi, diag, device,
-                                                         st);
+        return dispatch_fused_md<FP, LAYOUT, FK_MDIPOLE, PUSHER>(e, fa, co, n_steps, multi, diag,
+                                                                 device, st);
     case FK_GRID:
-        return dispatch_fused_md<FP, LAYOUT, FK_GRID>(e, fa, co, n_steps, multi, diag, device,
-                                                      st);
+        return dispatch_fused_md<FP, LAYOUT, FK_GRID, PUSHER>(e, fa, co, n_steps, multi, diag,
+                                                              device, st);
     default:
         return cudaErrorInvalidValue;
     }
 }
 
+template <typename FP, int LAYOUT>
+static cudaError_t dispatch_fused_pusher(const EnsView &e, int field_kind,
+                                         const AnalyticArgs<FP> &fa, const Coefs<FP> &co,
+                                         int64_t n_steps, bool multi, int pusher, DiagOut *diag,
+                                         int device, cudaStream_t st) {
+    switch (pusher) {
+    case PUSHER_VAY:
+        return dispatch_fused_field<FP, LAYOUT, PUSHER_VAY>(e, field_kind, fa, co, n_steps,
+                                                            multi, diag, device, st);
+    case PUSHER_HIGUERA_CARY:
+        return dispatch_fused_field<FP, LAYOUT, PUSHER_HIGUERA_CARY>(e, field_kind, fa, co,
+                                                                     n_steps, multi, diag,
+                                                                     device, st);
+    default:
+        return dispatch_fused_field<FP, LAYOUT, PUSHER_BORIS>(e, field_kind, fa, co, n_steps,
+                                                              multi, diag, device, st);
+    }
+}
+
 template <typename FP>
 cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,
-                         const Coefs<FP> &co, int64_t n_steps, bool multi, DiagOut *diag,
-                         int device, cudaStream_t st) {
+                         const Coefs<FP> &co, int64_t n_steps, bool multi, int pusher,
+                         DiagOut *diag, int device, cudaStream_t st) {
     if (e.n == 0) {
         if (diag) diag->written = 0;
         return cudaSuccess;
@@ -383,21 +413,21 @@ cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP
         DiagOut *d = (c0 + m == n_steps) ? diag : nullptr;
         const cudaError_t err =
             e.layout == BORIS_LAYOUT_SOA
-                ? dispatch_fused_field<FP, BORIS_LAYOUT_SOA>(e, field_kind, fc, co, m, multi, d,
-                                                             device, st)
-                : dispatch_fused_field<FP, BORIS_LAYOUT_AOS>(e, field_kind, fc, co, m, multi, d,
-                                                             device, st);
+                ? dispatch_fused_pusher<FP, BORIS_LAYOUT_SOA>(e, field_kind, fc, co, m, multi,
+                                                              pusher, d, device, st)
+                : dispatch_fused_pusher<FP, BORIS_LAYOUT_AOS>(e, field_kind, fc, co, m, multi,
+                                                              pusher, d, device, st);
         if (err != cudaSuccess) return err;
     }
     return cudaSuccess;
 }
 
 template cudaError_t launch_fused<float>(const EnsView &, int, const AnalyticArgs<float> &,
-                                         const Coefs<float> &, int64_t, bool, DiagOut *, int,
+                                         const Coefs<float> &, int64_t, bool, int, DiagOut *, int,
                                          cudaStream_t);
 template cudaError_t launch_fused<double>(const EnsView &, int, const AnalyticArgs<double> &,
-                                          const Coefs<double> &, int64_t, bool, DiagOut *, int,
-                                          cudaStream_t);
+                                          const Coefs<double> &, int64_t, bool, int, DiagOut *,
+                                          int, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // "Precalculated fields": an analytic field evaluated at

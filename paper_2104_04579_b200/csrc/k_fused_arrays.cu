@@ -12,7 +12,7 @@
 
 namespace boris {
 
-template <typename FP, int LAYOUT, bool MULTI, bool DIAG>
+template <typename FP, int LAYOUT, bool MULTI, bool DIAG, int PUSHER>
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused_arrays(EnsView e, FieldSoaPtrs f, const void *frec,
                    const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(kFusedThreads)
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
         FP ux = FP(0), uy = FP(0), uz = FP(0), gam = FP(1);
         for (int64_t s = 0; s < n_steps; ++s)
-            push_one<FP>(x, y, z, px, py, pz, gam, Ex, Ey, Ez, Bx, By, Bz, tc, ux, uy, uz);
+            push_one<FP, PUSHER>(x, y, z, px, py, pz, gam, Ex, Ey, Ez, Bx, By, Bz, tc, ux, uy,
+                                 uz);
         if (LAYOUT == BORIS_LAYOUT_SOA) {
             ((FP *)e.soa.x)[i] = x;
             ((FP *)e.soa.y)[i] = y;
@@ -75,50 +76,71 @@ __global__ void __launch_bounds__(kFusedThreads)
     if (DIAG) block_diag_partial<kFusedThreads>(ke, cnt, partials);
 }
 
-template <typename FP, int LAYOUT, bool MULTI, bool DIAG>
+template <typename FP, int LAYOUT, bool MULTI, bool DIAG, int PUSHER>
 static cudaError_t dispatch_fa(const EnsView &e, const FieldSoaPtrs &f, const void *frec,
                                const Coefs<FP> &co, int64_t n_steps, DiagOut *diag, int device,
                                cudaStream_t st) {
     const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    k_fused_arrays<FP, LAYOUT, MULTI, DIAG><<<(unsigned)grid, kFusedThreads, 0, st>>>(
+    k_fused_arrays<FP, LAYOUT, MULTI, DIAG, PUSHER><<<(unsigned)grid, kFusedThreads, 0, st>>>(
         e, f, frec, co, n_steps, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }
 
+template <typename FP, int LAYOUT, int PUSHER>
+static cudaError_t dispatch_fa_md(const EnsView &e, const FieldSoaPtrs &f, const void *frec,
+                                  const Coefs<FP> &co, int64_t n_steps, bool multi,
+                                  DiagOut *diag, int device, cudaStream_t st) {
+    if (multi)
+        return diag ? dispatch_fa<FP, LAYOUT, true, true, PUSHER>(e, f, frec, co, n_steps, diag,
+                                                                   device, st)
+                    : dispatch_fa<FP, LAYOUT, true, false, PUSHER>(e, f, frec, co, n_steps, diag,
+                                                                    device, st);
+    return diag ? dispatch_fa<FP, LAYOUT, false, true, PUSHER>(e, f, frec, co, n_steps, diag,
+                                                                device, st)
+                : dispatch_fa<FP, LAYOUT, false, false, PUSHER>(e, f, frec, co, n_steps, diag,
+                                                                 device, st);
+}
+
 template <typename FP, int LAYOUT>
 static cudaError_t dispatch_fa_layout(const EnsView &e, const FieldSoaPtrs &f, const void *frec,
                                       const Coefs<FP> &co, int64_t n_steps, bool multi,
-                                      DiagOut *diag, int device, cudaStream_t st) {
-    if (multi)
-        return diag ? dispatch_fa<FP, LAYOUT, true, true>(e, f, frec, co, n_steps, diag, device, st)
-                    : dispatch_fa<FP, LAYOUT, true, false>(e, f, frec, co, n_steps, diag, device, st);
-    return diag ? dispatch_fa<FP, LAYOUT, false, true>(e, f, frec, co, n_steps, diag, device, st)
-                : dispatch_fa<FP, LAYOUT, false, false>(e, f, frec, co, n_steps, diag, device, st);
+                                      int pusher, DiagOut *diag, int device, cudaStream_t st) {
+    switch (pusher) {
+    case PUSHER_VAY:
+        return dispatch_fa_md<FP, LAYOUT, PUSHER_VAY>(e, f, frec, co, n_steps, multi, diag,
+                                                      device, st);
+    case PUSHER_HIGUERA_CARY:
+        return dispatch_fa_md<FP, LAYOUT, PUSHER_HIGUERA_CARY>(e, f, frec, co, n_steps, multi,
+                                                               diag, device, st);
+    default:
+        return dispatch_fa_md<FP, LAYOUT, PUSHER_BORIS>(e, f, frec, co, n_steps, multi, diag,
+                                                        device, st);
+    }
 }
 
 template <typename FP>
 cudaError_t launch_fused_arrays(const EnsView &e, const FieldSoaPtrs &f, const void *frec,
-                                const Coefs<FP> &co, int64_t n_steps, bool multi,
+                                const Coefs<FP> &co, int64_t n_steps, bool multi, int pusher,
                                 DiagOut *diag, int device, cudaStream_t st) {
     if (e.n == 0) {
         if (diag) diag->written = 0;
         return cudaSuccess;
     }
     if (e.layout == BORIS_LAYOUT_SOA)
-        return dispatch_fa_layout<FP, BORIS_LAYOUT_SOA>(e, f, frec, co, n_steps, multi, diag,
-                                                        device, st);
-    return dispatch_fa_layout<FP, BORIS_LAYOUT_AOS>(e, f, frec, co, n_steps, multi, diag, device,
-                                                    st);
+        return dispatch_fa_layout<FP, BORIS_LAYOUT_SOA>(e, f, frec, co, n_steps, multi, pusher,
+                                                        diag, device, st);
+    return dispatch_fa_layout<FP, BORIS_LAYOUT_AOS>(e, f, frec, co, n_steps, multi, pusher, diag,
+                                                    device, st);
 }
 
 template cudaError_t launch_fused_arrays<float>(const EnsView &, const FieldSoaPtrs &,
                                                 const void *, const Coefs<float> &, int64_t, bool,
-                                                DiagOut *, int, cudaStream_t);
+                                                int, DiagOut *, int, cudaStream_t);
 template cudaError_t launch_fused_arrays<double>(const EnsView &, const FieldSoaPtrs &,
                                                  const void *, const Coefs<double> &, int64_t,
-                                                 bool, DiagOut *, int, cudaStream_t);
+                                                 bool, int, DiagOut *, int, cudaStream_t);
 
 }  // namespace boris

@@ -60,7 +60,8 @@ def oracle_field(w, precision, xi=None):
 class OracleRun:
     """The oracle's state for one workload, advanced in chunks like the GPU."""
 
-    def __init__(self, w, d, precision):
+    def __init__(self, w, d, precision, pusher=0):
+        self.pusher = pusher
         self.w = w
         self.pos = stack3(d, "x", "y", "z")
         self.mom = stack3(d, "px", "py", "pz")
@@ -80,7 +81,8 @@ class OracleRun:
     def push(self, n_steps):
         self.pos, self.mom, self.gamma = oracle.push(
             self.pos, self.mom, self.type, self.tq, self.tm, self.w.light_velocity, self.kind,
-            self.params, E=self.E, B=self.B, t0=self.t, dt=self.w.dt, n_steps=n_steps)
+            self.params, E=self.E, B=self.B, t0=self.t, dt=self.w.dt, n_steps=n_steps,
+            pusher=self.pusher)
         self.t += n_steps * self.w.dt
 
     def kinetic_energy(self):

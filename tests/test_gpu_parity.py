@@ -59,16 +59,19 @@ def gpu_state(ens):
             torch.stack([s["px"], s["py"], s["pz"]], 1).numpy(), s["gamma"].numpy(), s)
 
 
-def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False):
+ORACLE_PUSHER = {0: 0, lb.BORIS_PUSH_PUSHER_VAY: 1, lb.BORIS_PUSH_PUSHER_HIGUERA_CARY: 2}
+
+
+def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False, flags=0):
     d, ens, field = build(w, layout, precision, n, host=host)
-    ref = OracleRun(w, d, precision)
+    ref = OracleRun(w, d, precision, pusher=ORACLE_PUSHER[flags & lb.BORIS_PUSH_PUSHER_MASK])
     metric = C15()
     done = 0
     worst = {}
     stream = torch.cuda.current_stream()
     for s in checks:
         k = s - done
-        lb.boris_push(ens.handle, field, w.dt, k, stream)
+        lb.boris_push_ex(ens.handle, field, w.dt, k, flags, None, stream)
         ref.push(k)
         torch.cuda.synchronize()
         done = s
@@ -704,3 +707,56 @@ def test_sorted_push_equals_unsorted_push_bitwise():
         lb.boris_push(a.handle, h64, w.dt, 1)
     assert ei.value.status == lb.BORIS_E_MISMATCH
     lb.boris_field_destroy(h)
+
+
+# ---------------------------------------------------------------------------
+# Alternative pushers (readings c-vay, c-hc).
+# ---------------------------------------------------------------------------
+
+ALT_FLAGS = [lb.BORIS_PUSH_PUSHER_VAY, lb.BORIS_PUSH_PUSHER_HIGUERA_CARY]
+
+
+@pytest.mark.parametrize("flags", ALT_FLAGS)
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
+def test_alt_pusher_parity(flags, precision, cfg):
+    w = synth.config(cfg)
+    layout = "aos" if cfg == "C3" else "soa"
+    worst = run_parity(w, layout, precision, N_SMALL, flags=flags)
+    print(cfg, precision, hex(flags), worst)
+
+
+@pytest.mark.parametrize("flags", ALT_FLAGS)
+def test_alt_pusher_single_steps_equal_fused_bitwise(flags):
+    """Per-particle fields: n single-step launches == one n-step fused launch."""
+    w = synth.config("C2")
+    _, a, fa = build(w, "soa", "fp32", N_SMALL)
+    _, b, fb = build(w, "soa", "fp32", N_SMALL)
+    lb.boris_push_ex(a.handle, fa, w.dt, 5, flags)
+    lb.boris_push_ex(b.handle, fb, w.dt, 5, flags | lb.BORIS_PUSH_STREAM_EACH_STEP)
+    torch.cuda.synchronize()
+    sa, sb = a.state(), b.state()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(sa[k], sb[k]), k
+
+
+@pytest.mark.parametrize("flags", ALT_FLAGS)
+def test_alt_pusher_force_free_drift_on_gpu(flags):
+    """E x B drift at large dt: Vay / Higuera-Cary keep u = u_d (design property)."""
+    c, m, q = 1.0, 1.0, -1.0
+    bd = 0.9
+    ud = bd / math.sqrt(1 - bd * bd)
+    n = 1000
+    ens = SoaEnsemble(n, lb.BORIS_FP64, [(q, m)], c, with_fields=False)
+    ens.t["px"].fill_(ud * m * c)
+    ens.wrap()
+    f = lb.boris_field_create_uniform([0, bd, 0], [0, 0, 1])
+    lb.boris_push_ex(ens.handle, f, 2.0, 100, flags)
+    torch.cuda.synchronize()
+    s = ens.state()
+    assert (s["px"] / (m * c) - ud).abs().max().item() < 1e-12
+    assert s["py"].abs().max().item() < 1e-12
+    np.testing.assert_allclose(s["x"].numpy(), 100 * 2.0 * bd * c, rtol=1e-12)
+    with pytest.raises(lb.BorisError):
+        lb.boris_push_ex(ens.handle, f, 1.0, 1, lb.BORIS_PUSH_PUSHER_MASK)
+    lb.boris_field_destroy(f)

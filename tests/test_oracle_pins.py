@@ -575,3 +575,55 @@ def test_alt_pushers_converge_second_order_to_the_same_trajectory(pusher):
         Pb, Mb, _ = oracle.push(*args, E=E, B=B, dt=dt, n_steps=N, pusher=pusher)
         diffs.append(np.abs(Pb - Pa).max())
     assert 60 < diffs[0] / diffs[1] < 160, diffs
+
+
+# ---------------------------------------------------------------------------
+# Current deposition (reading c-dep): direct CIC at r^{n+1/2}.
+# ---------------------------------------------------------------------------
+
+def _vel(p, m, c):
+    m = np.asarray(m, dtype=float)
+    g = np.sqrt(1 + np.sum(p * p, -1) / (m * c) ** 2)
+    return p / (g * m)[..., None]
+
+
+def test_deposit_total_current_and_weights():
+    x0, y0, z0, dx, dy, dz, nx, ny, nz = GRID_P
+    vol = dx * dy * dz
+    rng = np.random.default_rng(31)
+    n = 500
+    pos = rng.normal(size=(n, 3)) * 4
+    mom = rng.normal(size=(n, 3)) * 2
+    w = rng.uniform(0.5, 1.5, n)
+    ty = rng.integers(0, 2, n).astype(np.int16)
+    tq, tm = [-1.0, 2.0], [1.0, 3.0]
+    c, dt = 1.0, 0.2
+    J = oracle.deposit_current(pos, mom, w, ty, tq, tm, c, dt, GRID_P)
+    v = _vel(mom, np.array(tm)[ty], c)
+    total = np.sum((np.array(tq)[ty] * w)[:, None] * v, 0)
+    # partition of unity: the grid holds exactly the total current sum q w v
+    np.testing.assert_allclose(J.reshape(3, -1).sum(1) * vol, total, rtol=1e-12, atol=1e-12)
+
+
+def test_deposit_half_step_position_and_cic_shares():
+    x0, y0, z0, dx, dy, dz, nx, ny, nz = GRID_P
+    vol = dx * dy * dz
+    c, dt, m, q = 1.0, 0.4, 1.0, -1.0
+    p = np.array([[0.3, -0.2, 0.5]])
+    v = _vel(p, m, c)[0]
+    node = np.array([x0 + 2 * dx, y0 + 3 * dy, z0 + 1 * dz])
+    # r^{n+1} chosen so that r^{n+1/2} = r^{n+1} - dt v/2 sits exactly on node (2, 3, 1)
+    J = oracle.deposit_current([node + 0.5 * dt * v], p, [1.0], [0], [q], [m], c, dt, GRID_P)
+    np.testing.assert_allclose(J[:, 1, 3, 2], q * v / vol, rtol=1e-12)
+    assert np.count_nonzero(np.abs(J) > 1e-14 * np.abs(J).max()) == 3
+    # half-step position at a cell centre: 1/8 of the current on each of the 8 nodes
+    centre = node + 0.5 * np.array([dx, dy, dz])
+    J = oracle.deposit_current([centre + 0.5 * dt * v], p, [1.0], [0], [q], [m], c, dt, GRID_P)
+    for kk in (1, 2):
+        for jj in (3, 4):
+            for ii in (2, 3):
+                np.testing.assert_allclose(J[:, kk, jj, ii], q * v / vol / 8, rtol=1e-12)
+    # periodic images deposit identically
+    J2 = oracle.deposit_current([centre + 0.5 * dt * v + [nx * dx, -2 * ny * dy, nz * dz]], p,
+                                [1.0], [0], [q], [m], c, dt, GRID_P)
+    np.testing.assert_allclose(J2, J, rtol=1e-12, atol=1e-15)
