@@ -262,6 +262,21 @@ boris_status boris_ensemble_sort_by_cell(boris_ensemble *ens, const boris_field 
                                          void *stream);
 
 /*
+ * Current deposition, the step after the push in a PIC cycle (
+ * "The grid values of the current J are computed and added to
+ * Maxwell's equations"; reading c-dep): for the state after a push of size dt
+ * (r^{n+1}, p^{n+1/2}), deposit q w v^{n+1/2} of every particle at its half-step
+ * position r^{n+1/2} = r^{n+1} - (dt/2) v^{n+1/2} onto the nodes of `grid` with the
+ * CIC form factor, divided by the cell volume (current density, statA/cm^2).
+ * Jx, Jy, Jz: DEVICE arrays of nx*ny*nz FP (node (i,j,k) at (k*ny+j)*nx+i), zeroed
+ * and then accumulated by this call.  Hardware atomics: the summation order
+ * varies run to run (results reproducible to rounding, not bitwise).
+ * Device ensembles; grid precision and device must match (MISMATCH).  Asynchronous.
+ */
+boris_status boris_deposit_current(const boris_ensemble *ens, const boris_field *grid, double dt,
+                                   void *Jx, void *Jy, void *Jz, void *stream);
+
+/*
  * "Precalculated fields" (L369-371, reading c6): evaluate the analytic field
  * `analytic` (uniform / plane wave / m-dipole) at every particle's current
  * position r_i at time t and write it into the per-particle field `out` (arrays

@@ -1073,6 +1073,51 @@ boris_status boris_field_create_grid(int32_t device, boris_precision precision, 
     return ok();
 }
 
+}  // extern "C"
+
+template <typename FP>
+static DepCoefs<FP> make_dep_coefs(const boris_ensemble *e, const boris_field *grid, double dt) {
+    DepCoefs<FP> dc;
+    memset(&dc, 0, sizeof dc);
+    dc.n_types = e->n_types;
+    dc.half_dt = (FP)(0.5 * dt);
+    const double vol = grid->h[0] * grid->h[1] * grid->h[2];
+    for (int i = 0; i < e->n_types; ++i) {
+        const double q = e->types[i].charge, m = e->types[i].mass, mc = m * e->c;
+        const double S = std::ldexp(1.0, -(int)std::lround(std::log2(mc)));
+        dc.t[i].S = (FP)S;
+        dc.t[i].kappa2 = (FP)(1.0 / ((S * mc) * (S * mc)));
+        dc.t[i].inv_Sm = (FP)(1.0 / (S * m));
+        dc.t[i].q_vol = (FP)(q / vol);
+    }
+    return dc;
+}
+
+extern "C" {
+
+boris_status boris_deposit_current(const boris_ensemble *e, const boris_field *grid, double dt,
+                                   void *Jx, void *Jy, void *Jz, void *stream) {
+    if (!e || !grid || !Jx || !Jy || !Jz) return fail(BORIS_E_INVALID_ARG, "NULL argument");
+    if (grid->kind != FK_GRID) return fail(BORIS_E_INVALID_ARG, "field is not a grid");
+    if (!std::isfinite(dt)) return fail(BORIS_E_INVALID_ARG, "dt must be finite");
+    if (grid->precision != e->precision || grid->device != e->device)
+        return fail(BORIS_E_MISMATCH, "grid and ensemble differ in precision or device");
+    if (e->memory != BORIS_MEMORY_DEVICE)
+        return fail(BORIS_E_UNSUPPORTED, "deposition needs a device-resident ensemble");
+    DeviceGuard g(e->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    cudaError_t err =
+        e->precision == BORIS_FP32
+            ? launch_deposit<float>(e->view(), make_grid_args<float>(grid),
+                                    make_dep_coefs<float>(e, grid, dt), Jx, Jy, Jz, e->device,
+                                    (cudaStream_t)stream)
+            : launch_deposit<double>(e->view(), make_grid_args<double>(grid),
+                                     make_dep_coefs<double>(e, grid, dt), Jx, Jy, Jz, e->device,
+                                     (cudaStream_t)stream);
+    if (err != cudaSuccess) return cuda_fail(err, "current deposition");
+    return ok();
+}
+
 boris_status boris_ensemble_sort_by_cell(boris_ensemble *e, const boris_field *grid,
                                          void *stream) {
     if (!e || !grid) return fail(BORIS_E_INVALID_ARG, "NULL argument");

@@ -92,6 +92,24 @@ cudaError_t launch_grid_pack(int precision, int64_t ncell, const void *const com
 template <typename FP>
 cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int device, cudaStream_t st);
 
+// Current deposition (reading c-dep): per-type coefficients.
+template <typename FP>
+struct DepCoef {
+    FP S;       // 2^k ~ 1/(mc): u = S p
+    FP kappa2;  // 1/(S m c)^2
+    FP inv_Sm;  // 1/(S m): v = u inv_Sm / gamma
+    FP q_vol;   // q / (hx hy hz)
+};
+template <typename FP>
+struct DepCoefs {
+    int n_types;
+    FP half_dt;
+    DepCoef<FP> t[kMaxTypes];
+};
+template <typename FP>
+cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
+                           void *Jx, void *Jy, void *Jz, int device, cudaStream_t st);
+
 // Analytic field at every particle's position (time baked into fa) -> arrays.
 template <typename FP>
 cudaError_t launch_field_evaluate(const EnsView &e, int field_kind, const AnalyticArgs<FP> &fa,

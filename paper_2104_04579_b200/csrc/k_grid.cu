@@ -274,6 +274,130 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     return err;
 }
 
+// ---------------------------------------------------------------------------
+// Current deposition (reading c-dep): direct CIC deposition
+// of q w v^{n+1/2} at r^{n+1/2} = r^{n+1} - (dt/2) v^{n+1/2}, divided by the cell
+// volume, with hardware float/double atomics (red.global.add) into J.
+// ---------------------------------------------------------------------------
+// Warp-aggregated scatter: lanes holding the same node in CONTIGUOUS lanes (the
+// common case for particles sorted by cell) are summed with a segmented shuffle
+// scan and only each segment's last lane issues the atomics.  Equal nodes in
+// non-contiguous lanes simply stay separate segments (still correct).
+constexpr uint32_t kNoNode = 0xFFFFFFFFu;
+
+template <typename FP>
+__device__ __forceinline__ void warp_scatter_add(uint32_t node, FP vx, FP vy, FP vz, FP *Jx,
+                                                 FP *Jy, FP *Jz) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t prev = __shfl_up_sync(full, node, 1);
+    const uint32_t next = __shfl_down_sync(full, node, 1);
+    const unsigned heads = __ballot_sync(full, lane == 0 || prev != node);
+    const int seg = 31 - __clz(heads & (full >> (31 - lane)));  // head lane of my segment
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const FP ax = __shfl_up_sync(full, vx, off);
+        const FP ay = __shfl_up_sync(full, vy, off);
+        const FP az = __shfl_up_sync(full, vz, off);
+        if (lane - off >= seg) {
+            vx = b_add(vx, ax);
+            vy = b_add(vy, ay);
+            vz = b_add(vz, az);
+        }
+    }
+    if ((lane == 31 || next != node) && node != kNoNode) {
+        atomicAdd(Jx + node, vx);
+        atomicAdd(Jy + node, vy);
+        atomicAdd(Jz + node, vz);
+    }
+}
+
+template <typename FP>
+__global__ void __launch_bounds__(256)
+    k_deposit(EnsView e, const __grid_constant__ GridArgs<FP> g,
+              const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz) {
+    constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // whole blocks iterate together so every lane takes part in the warp shuffles
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < e.n; base += stride) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < e.n;
+        FP x = FP(0), y = FP(0), z = FP(0), px = FP(0), py = FP(0), pz = FP(0), w = FP(0);
+        int ty = 0;
+        if (valid) {
+            if (e.layout == BORIS_LAYOUT_SOA) {
+                x = ((const FP *)e.soa.x)[i];
+                y = ((const FP *)e.soa.y)[i];
+                z = ((const FP *)e.soa.z)[i];
+                px = ((const FP *)e.soa.px)[i];
+                py = ((const FP *)e.soa.py)[i];
+                pz = ((const FP *)e.soa.pz)[i];
+                w = e.soa.w ? ((const FP *)e.soa.w)[i] : FP(1);
+                if (e.soa.type) ty = e.soa.type[i];
+            } else {
+                const FP *r = (const FP *)((const unsigned char *)e.aos + i * RB);
+                x = r[0]; y = r[1]; z = r[2];
+                px = r[3]; py = r[4]; pz = r[5];
+                w = r[6];
+                ty = *(const int16_t *)(r + 8);
+            }
+        }
+        const DepCoef<FP> t = dc.t[dc.n_types > 1 ? ty : 0];
+        const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
+        // v = p/(gamma m) = u/(S m gamma)
+        const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
+        const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
+        // half-step position
+        const FP xh = b_fma(-dc.half_dt, vx, x), yh = b_fma(-dc.half_dt, vy, y),
+                 zh = b_fma(-dc.half_dt, vz, z);
+        int ix[2], iy[2], iz[2];
+        FP fx, fy, fz;
+        grid_axis<FP>(xh, g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0], g.n[0], ix[0], ix[1], fx);
+        grid_axis<FP>(yh, g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1], g.n[1], iy[0], iy[1], fy);
+        grid_axis<FP>(zh, g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2], g.n[2], iz[0], iz[1], fz);
+        const FP wx[2] = {b_add(FP(1), -fx), fx};
+        const FP wy[2] = {b_add(FP(1), -fy), fy};
+        const FP wz[2] = {b_add(FP(1), -fz), fz};
+        const FP qw = b_mul(t.q_vol, w);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const FP wyz = b_mul(qw, b_mul(wy[b], wz[c]));
+                const uint32_t row =
+                    ((uint32_t)iz[c] * (uint32_t)g.n[1] + (uint32_t)iy[b]) * (uint32_t)g.n[0];
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const FP s = b_mul(wx[a], wyz);
+                    const uint32_t node = valid ? row + (uint32_t)ix[a] : kNoNode;
+                    warp_scatter_add<FP>(node, b_mul(s, vx), b_mul(s, vy), b_mul(s, vz), Jx, Jy,
+                                         Jz);
+                }
+            }
+    }
+}
+
+template <typename FP>
+cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
+                           void *Jx, void *Jy, void *Jz, int device, cudaStream_t st) {
+    const int64_t ncell = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    cudaError_t err = cudaMemsetAsync(Jx, 0, (size_t)ncell * sizeof(FP), st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(Jy, 0, (size_t)ncell * sizeof(FP), st);
+    if (err == cudaSuccess) err = cudaMemsetAsync(Jz, 0, (size_t)ncell * sizeof(FP), st);
+    if (err != cudaSuccess || e.n == 0) return err;
+    const int64_t blocks = (e.n + 255) / 256;
+    const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
+    k_deposit<FP><<<grid, 256, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz);
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_deposit<float>(const EnsView &, const GridArgs<float> &,
+                                           const DepCoefs<float> &, void *, void *, void *, int,
+                                           cudaStream_t);
+template cudaError_t launch_deposit<double>(const EnsView &, const GridArgs<double> &,
+                                            const DepCoefs<double> &, void *, void *, void *,
+                                            int, cudaStream_t);
+
 template cudaError_t sort_by_cell<float>(const EnsView &, const GridArgs<float> &, int,
                                          cudaStream_t);
 template cudaError_t sort_by_cell<double>(const EnsView &, const GridArgs<double> &, int,

@@ -709,6 +709,41 @@ def test_sorted_push_equals_unsorted_push_bitwise():
     lb.boris_field_destroy(h)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_deposit_current_vs_oracle(precision, layout):
+    """CIC current deposition at r^{n+1/2} (reading c-dep), generated state taken as the
+    post-push state; both sides deposit the same rounded inputs."""
+    h, params, gE, gB = grid_setup(precision)
+    w = synth.config("C5")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    n = N_SMALL
+    d = rounded(w.generate(0, n), precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    ens = cls(n, PREC[precision], w.types, w.light_velocity, with_fields=False)
+    ens.fill(d)
+    ens.wrap()
+    nx, ny, nz = int(params[6]), int(params[7]), int(params[8])
+    dt_ = torch.float32 if precision == "fp32" else torch.float64
+    J = [torch.full((nz, ny, nx), 7.0, dtype=dt_, device="cuda") for _ in range(3)]
+    lb.boris_deposit_current(ens.handle, h, w.dt, *(j.data_ptr() for j in J))
+    torch.cuda.synchronize()
+    Jg = torch.stack(J).double().cpu().numpy()
+    pos, mom = stack3(d, "x", "y", "z"), stack3(d, "px", "py", "pz")
+    tq, tm = [t[0] for t in w.types], [t[1] for t in w.types]
+    Jr = oracle.deposit_current(pos, mom, d["weight"].numpy(), d["type"].numpy(), tq, tm,
+                                w.light_velocity, w.dt, params)
+    scale = np.abs(Jr).max()
+    tol = 1e-5 if precision == "fp32" else 1e-12
+    assert np.abs(Jg - Jr).max() <= tol * scale
+    vol = params[3] * params[4] * params[5]
+    np.testing.assert_allclose(Jg.reshape(3, -1).sum(1) * vol, Jr.reshape(3, -1).sum(1) * vol,
+                               rtol=tol, atol=tol * scale * vol)
+    lb.boris_field_destroy(h)
+    ens.close()
+
+
 # ---------------------------------------------------------------------------
 # Alternative pushers (SURVEY §8(f) row 4; readings c-vay, c-hc).
 # ---------------------------------------------------------------------------
