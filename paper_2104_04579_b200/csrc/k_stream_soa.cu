@@ -167,12 +167,32 @@ static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const C
     return cudaGetLastError();
 }
 
+// Kernel selection for SoA streaming: "ldg" (default, k_stream_soa_vec) or "tma"
+// (k_stream_soa_tma); BORIS_SOA_KERNEL overrides.  Both are bitwise identical.
+static bool use_tma_soa() {
+    static int v = -1;
+    if (v < 0) {
+        const char *s = getenv("BORIS_SOA_KERNEL");
+        v = (s && s[0] == 't') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 template <typename FP>
 cudaError_t launch_stream_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
                               bool multi, DiagOut *diag, int device, cudaStream_t st) {
     if (e.n == 0) {
         if (diag) diag->written = 0;
         return cudaSuccess;
+    }
+    if (use_tma_soa()) {
+        const bool al = aligned16(e.soa.x) && aligned16(e.soa.y) && aligned16(e.soa.z) &&
+                        aligned16(e.soa.px) && aligned16(e.soa.py) && aligned16(e.soa.pz) &&
+                        aligned16(e.soa.g) && aligned16(f.Ex) && aligned16(f.Ey) &&
+                        aligned16(f.Ez) && aligned16(f.Bx) && aligned16(f.By) &&
+                        aligned16(f.Bz) && (!diag || !e.soa.w || aligned16(e.soa.w)) &&
+                        (!multi || aligned16(e.soa.type));
+        if (al) return launch_stream_soa_tma<FP>(e, f, co, multi, diag, device, st);
     }
     const bool d = diag != nullptr;
     if (multi)

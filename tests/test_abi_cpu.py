@@ -47,6 +47,17 @@ def test_library_is_sm100a(lb):
     assert "sm_100a" in out
 
 
+def test_sass_evidence(lb):
+    """The compiled sm_100a code uses what DESIGN.md claims: 128-bit streaming loads
+    (LDG.E.128), evict-first stores (STG.E.EF.128), TMA bulk copies with mbarrier
+    transaction counting (UBLKCP, SYNCS.ARRIVE.TRANS64) and MUFU rsqrt."""
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lb.LIB_PATH],
+                          capture_output=True, text=True, check=True).stdout
+    for op in ("LDG.E.NA.128", "LDG.E.NA.128.CONSTANT", "STG.E.EF.128", "UBLKCP.S.G",
+               "UBLKCP.G.S", "SYNCS.ARRIVE.TRANS64", "MUFU.RSQ", "MUFU.COS"):
+        assert op in sass, op
+
+
 def test_abi_version_and_status_strings(lb):
     assert lb.boris_abi_version() == 1
     for code, name in [(0, "BORIS_OK"), (1, "BORIS_E_INVALID_ARG"), (5, "BORIS_E_MISMATCH"),
