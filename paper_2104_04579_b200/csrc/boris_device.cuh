@@ -300,41 +300,55 @@ __device__ __forceinline__ FP kinetic_energy(FP ux, FP uy, FP uz, FP gamma, FP w
 // Nothing is reused within a step, so loads bypass L1 and stores are
 // evict-first (st.global.cs).
 // ---------------------------------------------------------------------------
+// Tuning knobs (experiments only; defaults are the measured best):
+// BORIS_LD_L2PF adds the .L2::256B prefetch-size hint to streaming loads,
+// BORIS_ST_WB uses write-back instead of evict-first (.cs) stores.
+#ifdef BORIS_LD_L2PF
+#define BORIS_LD_PF ".L2::256B"
+#else
+#define BORIS_LD_PF ""
+#endif
+#ifdef BORIS_ST_WB
+#define BORIS_ST_Q ""
+#else
+#define BORIS_ST_Q ".cs"
+#endif
+
 __device__ __forceinline__ float4 ld_state(const float *p) {
     float4 v;
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate" BORIS_LD_PF ".v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p));
     return v;
 }
 __device__ __forceinline__ double2 ld_state(const double *p) {
     double2 v;
-    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+    asm volatile("ld.global.L1::no_allocate" BORIS_LD_PF ".v2.f64 {%0,%1}, [%2];"
                  : "=d"(v.x), "=d"(v.y)
                  : "l"(p));
     return v;
 }
 __device__ __forceinline__ float4 ld_field(const float *p) {
     float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate" BORIS_LD_PF ".v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p));
     return v;
 }
 __device__ __forceinline__ double2 ld_field(const double *p) {
     double2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+    asm volatile("ld.global.nc.L1::no_allocate" BORIS_LD_PF ".v2.f64 {%0,%1}, [%2];"
                  : "=d"(v.x), "=d"(v.y)
                  : "l"(p));
     return v;
 }
 __device__ __forceinline__ void st_stream(float *p, float4 v) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+    asm volatile("st.global" BORIS_ST_Q ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w)
                  : "memory");
 }
 __device__ __forceinline__ void st_stream(double *p, double2 v) {
-    asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+    asm volatile("st.global" BORIS_ST_Q ".v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
 // Vector of the particles one thread owns: 4 floats or 2 doubles = 16 B.

@@ -11,7 +11,10 @@
 
 namespace boris {
 
-constexpr int kStreamThreads = 256;  // SoA streaming kernel block size
+#ifndef BORIS_STREAM_THREADS
+#define BORIS_STREAM_THREADS 256
+#endif
+constexpr int kStreamThreads = BORIS_STREAM_THREADS;  // SoA streaming kernel block size
 constexpr int kAosThreads = 256;     // AoS tile kernel block size (one particle / thread / tile)
 constexpr int kFusedThreads = 128;   // register-fused multi-step kernel block size
 constexpr int kFinalizeThreads = 1024;
