@@ -79,6 +79,38 @@ def main():
         lb.boris_ensemble_upload(h, 0, n, pos, pos * 1e-17, np.ones(n), np.zeros(n, np.int16))
         lb.boris_ensemble_download(h, 0, n)
         lb.boris_ensemble_destroy(h)
+    # grid gather push, sort by cell, deposition, alternative pushers (NEXT rows 3-4)
+    for prec in (lb.BORIS_FP32, lb.BORIS_FP64):
+        dt = torch.float32 if prec == lb.BORIS_FP32 else torch.float64
+        g = 5
+        L = 1.5 * synth.LAMBDA0
+        comps = [torch.randn((g, g + 1, g + 2), device="cuda", dtype=torch.float64).to(dt)
+                 * synth.E_UNIT for _ in range(6)]
+        grid = lb.boris_field_create_grid(0, prec, g + 2, g + 1, g, [-L / 2] * 3,
+                                          [L / (g + 2), L / (g + 1), L / g],
+                                          *(c.data_ptr() for c in comps))
+        J = [torch.zeros((g, g + 1, g + 2), device="cuda", dtype=dt) for _ in range(3)]
+        for n in (13, 3 * 2048 + 77):
+            w = synth.config("C2", n=n)
+            w.types = THREE
+            w.type_mix = "random"
+            for cls in (SoaEnsemble, AosEnsemble):
+                e = cls(n, prec, THREE, w.light_velocity)
+                e.fill(w.generate())
+                e.wrap()
+                lb.boris_ensemble_sort_by_cell(e.handle, grid)
+                lb.boris_push_diag(e.handle, grid, w.dt, 3, dp)
+                lb.boris_deposit_current(e.handle, grid, w.dt, *(j.data_ptr() for j in J))
+                lb.boris_field_evaluate(grid, e.handle, 0.0, e.field)
+                for flags in (lb.BORIS_PUSH_PUSHER_VAY, lb.BORIS_PUSH_PUSHER_HIGUERA_CARY):
+                    lb.boris_push_ex(e.handle, e.field, w.dt, 2, flags, dp)
+                    lb.boris_push_ex(e.handle, grid, w.dt, 2, flags, dp)
+                    f = analytic("plane_wave")
+                    lb.boris_push_ex(e.handle, f, w.dt, 2, flags, dp)
+                    lb.boris_field_destroy(f)
+                torch.cuda.synchronize()
+                e.close()
+        lb.boris_field_destroy(grid)
     # host-resident pipeline, several chunks
     os.environ["BORIS_HOST_CHUNK"] = "2048"
     w = synth.config("C5", n=5000)
