@@ -18,6 +18,12 @@ fi
 if [ $what = deposit ] || [ $what = all ]; then
   timeout 600 python scripts/bench_deposit.py > gpurun_out/extras/bench_deposit.jsonl 2> gpurun_out/extras/bench_deposit.err; echo deposit rc=$?
 fi
+if [ $what = pic ] || [ $what = all ]; then
+  for se in 1 10 1000000; do
+    timeout 600 python scripts/pic_cycle.py --sort-every $se >> gpurun_out/extras/pic_cycle.jsonl 2>> gpurun_out/extras/pic_cycle.err
+  done
+  echo pic rc=$?
+fi
 if [ $what = ncu ] || [ $what = all ]; then
   run() {  # name case kernel-regex skip
     timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"$3" -s $4 -c 1 \

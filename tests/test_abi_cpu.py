@@ -58,6 +58,27 @@ def test_sass_evidence(lb):
         assert op in sass, op
 
 
+def build_c_example(lb, tmp_path):
+    exe = tmp_path / "push_c_abi"
+    pkg = os.path.dirname(lb.LIB_PATH)
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "push_c_abi.c"), "-L", pkg, "-lboris",
+                           f"-Wl,-rpath,{pkg}", "-lm", "-o", str(exe)])
+    return exe
+
+
+def test_c_example_links_against_the_abi(lb, tmp_path):
+    """A plain C program compiles against include/libboris.h and links libboris.so;
+    without a GPU it stops at boris_ensemble_create with BORIS_E_NO_DEVICE (exit 2)."""
+    import torch
+    exe = build_c_example(lb, tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present (tests/test_gpu_parity.py runs it)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 2, r.stdout + r.stderr
+    assert "no CUDA device" in r.stdout
+
+
 def test_abi_version_and_status_strings(lb):
     assert lb.boris_abi_version() == 1
     for code, name in [(0, "BORIS_OK"), (1, "BORIS_E_INVALID_ARG"), (5, "BORIS_E_MISMATCH"),

@@ -467,6 +467,16 @@ def test_host_resident_analytic_multistep():
     run_parity(w, "soa", "fp64", N_SMALL, checks=(5, 20), host=True)
 
 
+def test_c_example_program(tmp_path):
+    """examples/push_c_abi.c: the C ABI used from plain C on the GPU (Larmor invariants)."""
+    import subprocess
+    from test_abi_cpu import build_c_example
+    exe = build_c_example(lb, tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "pushed 1000 electrons" in r.stdout
+
+
 def test_edge_cases_and_errors():
     w = synth.config("C2")
     # n = 0 ensembles and n_steps = 0 pushes are no-ops
