@@ -308,6 +308,10 @@ boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensem
  * step when n_steps == 1, one register-fused launch otherwise (bitwise the
  * same, see boris_push_ex); analytic fields -> one register-fused launch for
  * all n_steps.
+ * Device-ensemble pushes do no host synchronisation and no allocation, so they
+ * can be captured into a CUDA graph (after one eager call); note that the field
+ * time t0 and dt are baked into the captured kernel parameters, so replays of a
+ * captured analytic-field push re-use the captured times.
  * Host ensembles: the ensemble (and per-particle fields) stream through the
  * GPU in chunks with H2D / compute / D2H overlapped; each chunk is pushed all
  * n_steps while resident.  Host arrays must be pinned for asynchrony.

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                                       (fa.ph0 - (double)s0 * fa.wdt));
             FP dx = FP(0), dy = FP(0), dz = FP(0);
             const int m = (n_steps - s0) < kFlush ? (int)(n_steps - s0) : kFlush;
-            for (int j = 0; j < m; ++j) {
+            auto step = [&](int j) {
                 FP inv_g;
                 if constexpr (FIELD == FK_UNIFORM) {
                     if constexpr (PUSHER == PUSHER_BORIS)
@@ -308,6 +308,15 @@ __global__ void __launch_bounds__(kFusedThreads)
                 dx = b_fma(ct, ux, dx);
                 dy = b_fma(ct, uy, dy);
                 dz = b_fma(ct, uz, dz);
+            };
+            // full windows of the short-bodied fields run as straight-line code (measured
+            // +4 % on C4); the long m-dipole / grid bodies stay rolled (unrolled: -15 %).
+            constexpr bool kUnroll = FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE;
+            if (kUnroll && m == kFlush) {
+#pragma unroll
+                for (int j = 0; j < kFlush; ++j) step(j);
+            } else {
+                for (int j = 0; j < m; ++j) step(j);
             }
             xa = __dadd_rn(xa, (double)dx);
             ya = __dadd_rn(ya, (double)dy);

@@ -467,6 +467,34 @@ def test_host_resident_analytic_multistep():
     run_parity(w, "soa", "fp64", N_SMALL, checks=(5, 20), host=True)
 
 
+def test_push_is_cuda_graph_capturable():
+    """boris_push / boris_push_diag do no host sync or allocation: a step loop can be
+    captured once into a CUDA graph and replayed; replay == eager, bitwise."""
+    w = synth.config("C5", n=N_SMALL)
+    _, a, fa = build(w, "soa", "fp32")
+    _, b, fb = build(w, "soa", "fp32")
+    da = torch.zeros(2, dtype=torch.float64, device="cuda")
+    db = torch.zeros(2, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        lb.boris_push_diag(b.handle, fb, w.dt, 1, db.data_ptr(), s)   # warm-up (kernel attrs)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(4):
+            lb.boris_push_diag(b.handle, fb, w.dt, 1, db.data_ptr(), torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    for _ in range(1 + 4 * 2):   # eager: 1 warm-up step + 2 replays x 4 steps
+        lb.boris_push_diag(a.handle, fa, w.dt, 1, da.data_ptr())
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    sa, sb = a.state(), b.state()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(sa[k], sb[k]), k
+    assert torch.equal(da, db)
+
+
 def test_c_example_program(tmp_path):
     """examples/push_c_abi.c: the C ABI used from plain C on the GPU (Larmor invariants)."""
     import subprocess
