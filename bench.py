@@ -341,7 +341,8 @@ def main():
                        f"({bpp * n_local / 1e9:.1f} GB per GPU per step vs 126 MB)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_kind": peak_kind, "kernel": "k_stream_soa_vec<float,false,true>",
+                         "peak_kind": peak_kind, "frac_of_nominal_8tbs": achieved / 8000.0,
+                         "kernel": "k_stream_soa_vec<float,false,true>",
                          "bytes_per_particle": bpp},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -627,3 +627,21 @@ def test_deposit_half_step_position_and_cic_shares():
     J2 = oracle.deposit_current([centre + 0.5 * dt * v + [nx * dx, -2 * ny * dy, nz * dz]], p,
                                 [1.0], [0], [q], [m], c, dt, GRID_P)
     np.testing.assert_allclose(J2, J, rtol=1e-12, atol=1e-15)
+
+
+def test_oracle_under_address_and_undefined_behaviour_sanitizers(tmp_path):
+    """the oracle's every entry point runs clean under
+    -fsanitize=address,undefined (tests/oracle_sanitize_driver.c)."""
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+    exe = tmp_path / "oracle_san"
+    subprocess.check_call(["gcc", "-std=c11", "-O1", "-g", "-fsanitize=address,undefined",
+                           "-fno-sanitize-recover=all", "-fopenmp", "-I",
+                           os.path.join(root, "oracle"), os.path.join(here,
+                                                                     "oracle_sanitize_driver.c"),
+                           os.path.join(root, "oracle", "boris_oracle.c"), "-lm", "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True,
+                       env=dict(os.environ, ASAN_OPTIONS="detect_leaks=1"))
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "runtime error" not in r.stderr and "ERROR: AddressSanitizer" not in r.stderr
