@@ -76,7 +76,7 @@ size_t field_record_bytes(int precision) {
 // Handles
 // ---------------------------------------------------------------------------
 struct HostPipeline {
-    static constexpr int kBuffers = 2;
+    static constexpr int kBuffers = 3;  // H2D of chunk k+2 overlaps push k+1 and D2H k
     int64_t chunk = 0;
     void *dev_block[kBuffers] = {};
     SoaPtrs soa[kBuffers] = {};
@@ -351,6 +351,12 @@ cudaError_t push_view(const boris_ensemble *e, const EnsView &v, const boris_fie
         return cudaSuccess;
     }
     const AnalyticArgs<FP> fa = make_analytic<FP>(f, t0, dt);
+    if (f->kind == FK_GRID && n_steps == 1 && v.layout == BORIS_LAYOUT_SOA &&
+        pusher == PUSHER_BORIS) {  // the PIC single step: 128-bit streaming + gather
+        const cudaError_t err =
+            launch_stream_soa_grid<FP>(v, fa.grid, co, e->multi(), diag, e->device, st);
+        if (err != cudaErrorNotSupported) return err;
+    }
     return launch_fused<FP>(v, f->kind, fa, co, n_steps, e->multi(), pusher, diag, e->device, st);
 }
 

@@ -78,6 +78,12 @@ template <typename FP>
 cudaError_t launch_stream_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
                               bool multi, DiagOut *diag, int device, cudaStream_t st);
 
+// Single-step SoA push with a grid-gathered field (cudaErrorNotSupported if the
+// arrays are not 16 B aligned).
+template <typename FP>
+cudaError_t launch_stream_soa_grid(const EnsView &e, const GridArgs<FP> &g, const Coefs<FP> &co,
+                                   bool multi, DiagOut *diag, int device, cudaStream_t st);
+
 template <typename FP>
 cudaError_t launch_stream_soa_tma(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
                                   bool multi, DiagOut *diag, int device, cudaStream_t st);

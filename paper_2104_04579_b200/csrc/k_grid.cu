@@ -377,6 +377,130 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Run-accumulating deposition (SoA): each lane deposits K consecutive particles,
+// keeping the 8 nodes x 3 components of its current cell in registers and
+// issuing atomics only when the cell changes.  For particles sorted by cell
+// (boris_ensemble_sort_by_cell) one flush covers a whole run.  Warp tiles are
+// staged through shared memory with coalesced loads and a skewed layout
+// (p -> p + p/K) so the per-lane sequential reads are bank-conflict free.
+// ---------------------------------------------------------------------------
+template <typename FP>
+struct DepRuns {
+    static constexpr int K = 8;          // particles per lane per tile
+    static constexpr int WARPS = sizeof(FP) == 4 ? 4 : 2;  // <= 48 KB static smem
+    static constexpr int TILE = 32 * K;  // particles per warp tile
+    static constexpr int SK = TILE + TILE / K;
+};
+
+static bool deposit_runs_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *s = getenv("BORIS_DEPOSIT_KERNEL");
+        v = (s && s[0] == 'w') ? 0 : 1;  // "warp" selects the warp-scan kernel
+    }
+    return v == 1;
+}
+
+template <typename FP>
+__global__ void __launch_bounds__(DepRuns<FP>::WARPS * 32)
+    k_deposit_runs(EnsView e, const __grid_constant__ GridArgs<FP> g,
+                   const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz) {
+    using R = DepRuns<FP>;
+    __shared__ FP s[R::WARPS][7][R::SK];
+    __shared__ int16_t s_ty[R::WARPS][R::SK];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const FP *arr[7] = {(const FP *)e.soa.x, (const FP *)e.soa.y, (const FP *)e.soa.z,
+                        (const FP *)e.soa.px, (const FP *)e.soa.py, (const FP *)e.soa.pz,
+                        (const FP *)e.soa.w};
+    const bool multi = dc.n_types > 1 && e.soa.type;
+    const int64_t stride = (int64_t)gridDim.x * R::WARPS * R::TILE;
+    for (int64_t base = ((int64_t)blockIdx.x * R::WARPS + warp) * R::TILE; base < e.n;
+         base += stride) {
+        // coalesced warp loads into the skewed tile
+#pragma unroll
+        for (int r = 0; r < R::K; ++r) {
+            const int p = r * 32 + lane;
+            const int64_t i = base + p;
+            const int sp = p + p / R::K;
+#pragma unroll
+            for (int a = 0; a < 7; ++a)
+                s[warp][a][sp] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
+            if (multi) s_ty[warp][sp] = (i < e.n) ? e.soa.type[i] : (int16_t)0;
+        }
+        __syncwarp();
+        FP acc[8][3];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+        int cx[2] = {-1, -1}, cy[2] = {0, 0}, cz[2] = {0, 0};
+        auto flush = [&]() {
+            if (cx[0] < 0) return;
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const uint32_t row =
+                        ((uint32_t)cz[c] * (uint32_t)g.n[1] + (uint32_t)cy[b]) * (uint32_t)g.n[0];
+#pragma unroll
+                    for (int a = 0; a < 2; ++a) {
+                        const int q = (c * 2 + b) * 2 + a;
+                        const uint32_t node = row + (uint32_t)cx[a];
+                        atomicAdd(Jx + node, acc[q][0]);
+                        atomicAdd(Jy + node, acc[q][1]);
+                        atomicAdd(Jz + node, acc[q][2]);
+                        acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+                    }
+                }
+        };
+        for (int j = 0; j < R::K; ++j) {
+            const int p = lane * R::K + j;
+            if (base + p >= e.n) break;
+            const int sp = p + p / R::K;
+            const FP x = s[warp][0][sp], y = s[warp][1][sp], z = s[warp][2][sp];
+            const FP px = s[warp][3][sp], py = s[warp][4][sp], pz = s[warp][5][sp];
+            const FP w = s[warp][6][sp];
+            const DepCoef<FP> t = dc.t[multi ? s_ty[warp][sp] : 0];
+            const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
+            const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
+            const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
+            int ix[2], iy[2], iz[2];
+            FP fx, fy, fz;
+            grid_axis<FP>(b_fma(-dc.half_dt, vx, x), g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0],
+                          g.n[0], ix[0], ix[1], fx);
+            grid_axis<FP>(b_fma(-dc.half_dt, vy, y), g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1],
+                          g.n[1], iy[0], iy[1], fy);
+            grid_axis<FP>(b_fma(-dc.half_dt, vz, z), g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2],
+                          g.n[2], iz[0], iz[1], fz);
+            if (ix[0] != cx[0] || iy[0] != cy[0] || iz[0] != cz[0]) {
+                flush();
+                cx[0] = ix[0]; cx[1] = ix[1];
+                cy[0] = iy[0]; cy[1] = iy[1];
+                cz[0] = iz[0]; cz[1] = iz[1];
+            }
+            const FP wx[2] = {b_add(FP(1), -fx), fx};
+            const FP wy[2] = {b_add(FP(1), -fy), fy};
+            const FP wz[2] = {b_add(FP(1), -fz), fz};
+            const FP qw = b_mul(t.q_vol, w);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const FP wyz = b_mul(qw, b_mul(wy[b], wz[c]));
+#pragma unroll
+                    for (int a = 0; a < 2; ++a) {
+                        const int q = (c * 2 + b) * 2 + a;
+                        const FP sw = b_mul(wx[a], wyz);
+                        acc[q][0] = b_fma(sw, vx, acc[q][0]);
+                        acc[q][1] = b_fma(sw, vy, acc[q][1]);
+                        acc[q][2] = b_fma(sw, vz, acc[q][2]);
+                    }
+                }
+        }
+        flush();
+        __syncwarp();
+    }
+}
+
 template <typename FP>
 cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
                            void *Jx, void *Jy, void *Jz, int device, cudaStream_t st) {
@@ -385,6 +509,15 @@ cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoe
     if (err == cudaSuccess) err = cudaMemsetAsync(Jy, 0, (size_t)ncell * sizeof(FP), st);
     if (err == cudaSuccess) err = cudaMemsetAsync(Jz, 0, (size_t)ncell * sizeof(FP), st);
     if (err != cudaSuccess || e.n == 0) return err;
+    if (e.layout == BORIS_LAYOUT_SOA && deposit_runs_enabled()) {
+        using R = DepRuns<FP>;
+        const int64_t tiles = (e.n + R::TILE - 1) / R::TILE;
+        const int64_t blocks = (tiles + R::WARPS - 1) / R::WARPS;
+        const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
+        k_deposit_runs<FP><<<grid, R::WARPS * 32, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy,
+                                                            (FP *)Jz);
+        return cudaGetLastError();
+    }
     const int64_t blocks = (e.n + 255) / 256;
     const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
     k_deposit<FP><<<grid, 256, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz);

@@ -104,6 +104,129 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
     if (DIAG) block_diag_partial<kStreamThreads>(ke, cnt, partials);
 }
 
+// Single-step push with the field gathered from a grid (the
+// PIC case: the grid field changes between steps, so pushes are single steps).
+// Same 128-bit state streaming as k_stream_soa_vec; the V particles of a thread
+// gather their 8 nodes each with independent loads (ILP hides the L1/L2 latency).
+template <typename FP, bool MULTI, bool DIAG>
+__global__ void __launch_bounds__(kStreamThreads)
+    k_stream_soa_grid(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
+                      const __grid_constant__ Coefs<FP> co, int64_t n_groups, int64_t n,
+                      double *partials) {
+    constexpr int V = Vec<FP>::N;
+    __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    if (MULTI) load_type_table(co, s_t);
+    FP *X = (FP *)s.x, *Y = (FP *)s.y, *Z = (FP *)s.z;
+    FP *PX = (FP *)s.px, *PY = (FP *)s.py, *PZ = (FP *)s.pz, *G = (FP *)s.g;
+    const FP *W = (const FP *)s.w;
+    double ke = 0.0, cnt = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
+    for (int64_t grp = (int64_t)blockIdx.x * kStreamThreads + threadIdx.x; grp < n_groups;
+         grp += stride) {
+        const int64_t i0 = grp * V;
+        Vec<FP> x, y, z, px, py, pz, w, gm;
+        x.load_state(X + i0);
+        y.load_state(Y + i0);
+        z.load_state(Z + i0);
+        px.load_state(PX + i0);
+        py.load_state(PY + i0);
+        pz.load_state(PZ + i0);
+        int ty[V];
+        if (MULTI) load_types<V>(s.type + i0, ty);
+        if (DIAG) {
+            if (W) w.load_field(W + i0);
+            else {
+#pragma unroll
+                for (int j = 0; j < V; ++j) w.v[j] = FP(1);
+            }
+        }
+        FP ex[V], ey[V], ez[V], bx[V], by[V], bz[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            grid_gather<FP>(g, x.v[j], y.v[j], z.v[j], ex[j], ey[j], ez[j], bx[j], by[j], bz[j]);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const TypeCoef<FP> tc = MULTI ? s_t[ty[j]] : co.t[0];
+            FP ux, uy, uz;
+            push_one<FP>(x.v[j], y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], gm.v[j], ex[j], ey[j],
+                         ez[j], bx[j], by[j], bz[j], tc, ux, uy, uz);
+            if (DIAG) {
+                ke += (double)kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j], tc);
+                cnt += 1.0;
+            }
+        }
+        x.store(X + i0);
+        y.store(Y + i0);
+        z.store(Z + i0);
+        px.store(PX + i0);
+        py.store(PY + i0);
+        pz.store(PZ + i0);
+        gm.store(G + i0);
+    }
+    const int64_t tail0 = n_groups * V;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail0) {
+        const int64_t i = tail0 + threadIdx.x;
+        const TypeCoef<FP> tc = MULTI ? s_t[s.type[i]] : co.t[0];
+        FP ux, uy, uz, gam, Ex, Ey, Ez, Bx, By, Bz;
+        FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
+        grid_gather<FP>(g, x, y, z, Ex, Ey, Ez, Bx, By, Bz);
+        push_one<FP>(x, y, z, px, py, pz, gam, Ex, Ey, Ez, Bx, By, Bz, tc, ux, uy, uz);
+        X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
+        if (DIAG) {
+            ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, W ? W[i] : FP(1), tc);
+            cnt += 1.0;
+        }
+    }
+    if (DIAG) block_diag_partial<kStreamThreads>(ke, cnt, partials);
+}
+
+template <typename FP, bool MULTI, bool DIAG>
+static cudaError_t dispatch_soa_grid(const EnsView &e, const GridArgs<FP> &g,
+                                     const Coefs<FP> &co, DiagOut *diag, int device,
+                                     cudaStream_t st) {
+    constexpr int V = Vec<FP>::N;
+    const int64_t n_groups = e.n / V;
+    const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
+    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+    if (DIAG && grid > diag->cap) grid = diag->cap;
+    k_stream_soa_grid<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
+        e.soa, g, co, n_groups, e.n, diag ? diag->partials : nullptr);
+    if (diag) diag->written = DIAG ? grid : 0;
+    return cudaGetLastError();
+}
+
+static bool aligned16(const void *p);
+
+// Returns cudaErrorNotSupported when the arrays are not 16 B aligned (the caller
+// then uses the fused kernel).
+template <typename FP>
+cudaError_t launch_stream_soa_grid(const EnsView &e, const GridArgs<FP> &g, const Coefs<FP> &co,
+                                   bool multi, DiagOut *diag, int device, cudaStream_t st) {
+    constexpr int V = Vec<FP>::N;
+    if (e.n == 0) {
+        if (diag) diag->written = 0;
+        return cudaSuccess;
+    }
+    const bool al = aligned16(e.soa.x) && aligned16(e.soa.y) && aligned16(e.soa.z) &&
+                    aligned16(e.soa.px) && aligned16(e.soa.py) && aligned16(e.soa.pz) &&
+                    aligned16(e.soa.g) && (!diag || !e.soa.w || aligned16(e.soa.w)) &&
+                    (!multi || ((uintptr_t)e.soa.type & (2 * V - 1)) == 0);
+    if (!al) return cudaErrorNotSupported;
+    const bool d = diag != nullptr;
+    if (multi)
+        return d ? dispatch_soa_grid<FP, true, true>(e, g, co, diag, device, st)
+                 : dispatch_soa_grid<FP, true, false>(e, g, co, diag, device, st);
+    return d ? dispatch_soa_grid<FP, false, true>(e, g, co, diag, device, st)
+             : dispatch_soa_grid<FP, false, false>(e, g, co, diag, device, st);
+}
+
+template cudaError_t launch_stream_soa_grid<float>(const EnsView &, const GridArgs<float> &,
+                                                   const Coefs<float> &, bool, DiagOut *, int,
+                                                   cudaStream_t);
+template cudaError_t launch_stream_soa_grid<double>(const EnsView &, const GridArgs<double> &,
+                                                    const Coefs<double> &, bool, DiagOut *, int,
+                                                    cudaStream_t);
+
 // Unaligned inputs (e.g. sliced torch tensors): one particle per thread, scalar
 // accesses, the same push_one arithmetic.
 template <typename FP, bool MULTI, bool DIAG>
