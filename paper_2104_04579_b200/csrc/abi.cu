@@ -857,7 +857,7 @@ boris_status boris_ensemble_upload(boris_ensemble *e, int64_t first, int64_t cou
     const size_t c = (size_t)count;
     const size_t bytes = c * 8 * 8 + c * 2 + 64 * 8 + 256;
     unsigned char *d = nullptr;
-    CUDA_TRY(cudaMallocAsync((void **)&d, bytes, st), "cudaMallocAsync(upload staging)");
+    CUDA_TRY(scratch_alloc((void **)&d, bytes, st), "scratch_alloc(upload staging)");
     double *d_pos = (double *)d, *d_mom = d_pos + 3 * c, *d_w = d_mom + 3 * c, *d_g = d_w + c;
     double *d_inv = d_g + c;
     int16_t *d_type = (int16_t *)(d_inv + 64);
@@ -876,7 +876,7 @@ boris_status boris_ensemble_upload(boris_ensemble *e, int64_t first, int64_t cou
         err = launch_from_canonical(e->view(), first, count, d_pos, d_mom, d_w, d_type,
                                     gamma ? d_g : nullptr, d_inv, e->n_types, weight != nullptr,
                                     type != nullptr, st);
-    cudaFreeAsync(d, st);
+    scratch_free(d, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) return cuda_fail(err, "boris_ensemble_upload");
     return ok();
@@ -911,7 +911,7 @@ boris_status boris_ensemble_download(const boris_ensemble *e, int64_t first, int
     cudaStream_t st = (cudaStream_t)stream;
     const size_t c = (size_t)count;
     unsigned char *d = nullptr;
-    CUDA_TRY(cudaMallocAsync((void **)&d, c * 8 * 8 + c * 2 + 256, st), "cudaMallocAsync(download staging)");
+    CUDA_TRY(scratch_alloc((void **)&d, c * 8 * 8 + c * 2 + 256, st), "scratch_alloc(download staging)");
     double *d_pos = (double *)d, *d_mom = d_pos + 3 * c, *d_w = d_mom + 3 * c, *d_g = d_w + c;
     int16_t *d_type = (int16_t *)(d_g + c);
     cudaError_t err = launch_to_canonical(e->view(), first, count, d_pos, d_mom, d_w, d_g, d_type, st);
@@ -920,7 +920,7 @@ boris_status boris_ensemble_download(const boris_ensemble *e, int64_t first, int
     if (err == cudaSuccess && weight) err = cudaMemcpyAsync(weight, d_w, c * 8, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess && gamma) err = cudaMemcpyAsync(gamma, d_g, c * 8, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess && type) err = cudaMemcpyAsync(type, d_type, c * 2, cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(d, st);
+    scratch_free(d, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) return cuda_fail(err, "boris_ensemble_download");
     return ok();

@@ -308,6 +308,11 @@ __device__ __forceinline__ FP kinetic_energy(FP ux, FP uy, FP uz, FP gamma, FP w
 #else
 #define BORIS_LD_PF ""
 #endif
+#ifdef BORIS_STATE_NC
+#define BORIS_STATE_LD "ld.global.nc.L1::no_allocate"
+#else
+#define BORIS_STATE_LD "ld.global.L1::no_allocate"
+#endif
 #ifdef BORIS_ST_WB
 #define BORIS_ST_Q ""
 #else
@@ -316,14 +321,14 @@ __device__ __forceinline__ FP kinetic_energy(FP ux, FP uy, FP uz, FP gamma, FP w
 
 __device__ __forceinline__ float4 ld_state(const float *p) {
     float4 v;
-    asm volatile("ld.global.L1::no_allocate" BORIS_LD_PF ".v4.f32 {%0,%1,%2,%3}, [%4];"
+    asm volatile(BORIS_STATE_LD BORIS_LD_PF ".v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p));
     return v;
 }
 __device__ __forceinline__ double2 ld_state(const double *p) {
     double2 v;
-    asm volatile("ld.global.L1::no_allocate" BORIS_LD_PF ".v2.f64 {%0,%1}, [%2];"
+    asm volatile(BORIS_STATE_LD BORIS_LD_PF ".v2.f64 {%0,%1}, [%2];"
                  : "=d"(v.x), "=d"(v.y)
                  : "l"(p));
     return v;

@@ -71,6 +71,10 @@ struct DiagOut {
 
 int sm_count(int device);
 
+// Stream-ordered scratch from the library's per-device pool (k_util.cu).
+cudaError_t scratch_alloc(void **ptr, size_t bytes, cudaStream_t st);
+void scratch_free(void *ptr, cudaStream_t st);
+
 // Grid of a grid-stride launch: min(work blocks, SMs x resident blocks x waves).
 int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device);
 

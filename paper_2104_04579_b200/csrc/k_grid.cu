@@ -179,14 +179,14 @@ static cudaError_t exclusive_scan(uint32_t *data, int64_t len, cudaStream_t st) 
         return cudaGetLastError();
     }
     uint32_t *tot = nullptr;
-    cudaError_t err = cudaMallocAsync((void **)&tot, (size_t)chunks * sizeof(uint32_t), st);
+    cudaError_t err = scratch_alloc((void **)&tot, (size_t)chunks * sizeof(uint32_t), st);
     if (err != cudaSuccess) return err;
     k_scan_chunks<<<(unsigned)chunks, kScanThreads, 0, st>>>(data, len, tot);
     if ((err = exclusive_scan(tot, chunks, st)) == cudaSuccess) {
         k_scan_add<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(data, len, tot);
         err = cudaGetLastError();
     }
-    cudaFreeAsync(tot, st);
+    scratch_free(tot, st);
     return err;
 }
 
@@ -213,6 +213,22 @@ __global__ void k_gather_bytes(const unsigned char *in, unsigned char *out, cons
     }
 }
 
+// All SoA arrays at once: blk[a*fb + i] = arr_a[perm[i]] (perm read once per i).
+template <typename FP>
+__global__ void k_permute_soa(SoaPtrs s, const uint32_t *perm, int64_t n, unsigned char *blk,
+                              size_t fb) {
+    const FP *src[8] = {(const FP *)s.x, (const FP *)s.y, (const FP *)s.z, (const FP *)s.px,
+                        (const FP *)s.py, (const FP *)s.pz, (const FP *)s.w, (const FP *)s.g};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t j = perm[i];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+            if (src[a]) ((FP *)(blk + a * fb))[i] = src[a][j];
+        if (s.type) ((int16_t *)(blk + 8 * fb))[i] = s.type[j];
+    }
+}
+
 template <int BYTES>
 static cudaError_t permute_array(void *arr, void *tmp, const uint32_t *perm, int64_t n,
                                  cudaStream_t st) {
@@ -235,11 +251,11 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     const int passes = (bits + 7) / 8;
     const int64_t nb = (n + kRsTile - 1) / kRsTile;
     constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
-    const size_t tmp_bytes = (size_t)n * (e.layout == BORIS_LAYOUT_SOA ? sizeof(FP) : RB);
+    const size_t tmp_bytes = e.layout == BORIS_LAYOUT_SOA ? 0 : (size_t)n * RB;
     unsigned char *buf = nullptr;
     const size_t kv = (size_t)n * sizeof(uint32_t);
     const size_t hist_bytes = (size_t)256 * nb * sizeof(uint32_t);
-    cudaError_t err = cudaMallocAsync((void **)&buf, 4 * kv + hist_bytes + tmp_bytes + 256, st);
+    cudaError_t err = scratch_alloc((void **)&buf, 4 * kv + hist_bytes + tmp_bytes + 256, st);
     if (err != cudaSuccess) return err;
     uint32_t *k0 = (uint32_t *)buf, *v0 = k0 + n, *k1 = v0 + n, *v1 = k1 + n;
     uint32_t *hist = v1 + n;
@@ -261,16 +277,29 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     // v0 = sorted original indices: apply to every particle array
     if (err == cudaSuccess) {
         if (e.layout == BORIS_LAYOUT_SOA) {
-            void *arrs[8] = {e.soa.x, e.soa.y, e.soa.z, e.soa.px, e.soa.py, e.soa.pz, e.soa.w, e.soa.g};
-            for (int a = 0; a < 8 && err == cudaSuccess; ++a)
-                if (arrs[a]) err = permute_array<sizeof(FP)>(arrs[a], tmp, v0, n, st);
-            if (err == cudaSuccess && e.soa.type)
-                err = permute_array<2>(e.soa.type, tmp, v0, n, st);
+            // one gather kernel for all arrays into a scratch block, then copy back
+            unsigned char *blk = nullptr;
+            const size_t fb = ((size_t)n * sizeof(FP) + 255) / 256 * 256;
+            err = scratch_alloc((void **)&blk, 8 * fb + (size_t)n * 2 + 256, st);
+            if (err == cudaSuccess) {
+                k_permute_soa<FP><<<grid1d(n), 256, 0, st>>>(e.soa, v0, n, blk, fb);
+                err = cudaGetLastError();
+                void *arrs[8] = {e.soa.x, e.soa.y, e.soa.z, e.soa.px,
+                                 e.soa.py, e.soa.pz, e.soa.w, e.soa.g};
+                for (int a = 0; a < 8 && err == cudaSuccess; ++a)
+                    if (arrs[a])
+                        err = cudaMemcpyAsync(arrs[a], blk + a * fb, (size_t)n * sizeof(FP),
+                                              cudaMemcpyDeviceToDevice, st);
+                if (err == cudaSuccess && e.soa.type)
+                    err = cudaMemcpyAsync(e.soa.type, blk + 8 * fb, (size_t)n * 2,
+                                          cudaMemcpyDeviceToDevice, st);
+                scratch_free(blk, st);
+            }
         } else {
             err = permute_array<RB>(e.aos, tmp, v0, n, st);
         }
     }
-    cudaFreeAsync(buf, st);
+    scratch_free(buf, st);
     return err;
 }
 
@@ -495,6 +524,30 @@ __global__ void __launch_bounds__(DepRuns<FP>::WARPS * 32)
                         acc[q][2] = b_fma(sw, vz, acc[q][2]);
                     }
                 }
+        }
+        // End of tile: lanes still holding the same cell (contiguous when sorted) are
+        // summed with a warp segmented scan; only each segment's last lane flushes.
+        {
+            const unsigned full = 0xffffffffu;
+            const uint32_t key = cx[0] < 0 ? kNoNode
+                                           : ((uint32_t)cz[0] * (uint32_t)g.n[1] + (uint32_t)cy[0]) *
+                                                     (uint32_t)g.n[0] + (uint32_t)cx[0];
+            const uint32_t prev = __shfl_up_sync(full, key, 1);
+            const uint32_t next = __shfl_down_sync(full, key, 1);
+            const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
+            const int seg = 31 - __clz(heads & (full >> (31 - lane)));
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const bool take = lane - off >= seg;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const FP v = __shfl_up_sync(full, acc[q][d], off);
+                        if (take) acc[q][d] = b_add(acc[q][d], v);
+                    }
+            }
+            if (!(lane == 31 || next != key)) cx[0] = -1;  // not a segment tail: no flush
         }
         flush();
         __syncwarp();

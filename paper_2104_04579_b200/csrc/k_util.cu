@@ -16,6 +16,48 @@ int sm_count(int device) {
     return v;
 }
 
+// Stream-ordered scratch (sort keys, permutation blocks, staging) comes from one
+// library-owned pool per device whose release threshold keeps up to 1/16 of the
+// device memory cached across synchronisations: repeated sorts/uploads then reuse
+// mapped memory instead of re-mapping hundreds of MB per call.  The process's
+// default pool is left untouched.
+static cudaMemPool_t scratch_pool(int device) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    if (device < 0 || device >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[device]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        size_t total = 0, free_b = 0;
+        uint64_t keep = 1ull << 32;
+        if (cudaMemGetInfo(&free_b, &total) == cudaSuccess) keep = total / 16;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[device] = p;
+    }
+    return pools[device];
+}
+
+cudaError_t scratch_alloc(void **ptr, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    cudaMemPool_t pool = scratch_pool(dev);
+    if (!pool) return cudaMallocAsync(ptr, bytes, st);
+    return cudaMallocFromPoolAsync(ptr, bytes, pool, st);
+}
+
+void scratch_free(void *ptr, cudaStream_t st) {
+    if (ptr) cudaFreeAsync(ptr, st);
+}
+
 int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device) {
     // Grid-stride kernels: enough blocks for every SM to hold `blocks_per_sm`
     // resident blocks, times a few waves so the tail wave is short.

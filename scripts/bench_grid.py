@@ -55,15 +55,25 @@ def main():
         w = synth.config("C2", n=a.n)
         w.dt = synth.T0 / 1e4
         ens = SoaEnsemble(a.n, prec, w.types, w.light_velocity, with_fields=False)
-        ens.fill(w.generate(0, a.n, device="cuda"))
+        state0 = w.generate(0, a.n, device="cuda")
+        ens.fill(state0)
         ens.wrap()
         sp = torch.cuda.current_stream().cuda_stream
         for order in ("unsorted", "sorted"):
             if order == "sorted":
-                ms_sort = timed(lambda: lb.boris_ensemble_sort_by_cell(ens.handle, grid, sp), 3)
-                print(json.dumps({"exp": "sort_by_cell", "precision": prec_name, "n": a.n,
-                                  "cells": g ** 3, "ms": ms_sort,
-                                  "ns_per_particle": ms_sort * 1e6 / a.n}), flush=True)
+                # random order: refill the unsorted state before each timed sort
+                ts = []
+                for _ in range(4):
+                    ens.fill(state0)
+                    ts.append(timed(lambda: lb.boris_ensemble_sort_by_cell(ens.handle, grid, sp),
+                                    1, warmup=0))
+                ms_sort = statistics.median(ts[1:])
+                # already sorted (the periodic re-sort of a PIC loop is close to this)
+                ms_pre = timed(lambda: lb.boris_ensemble_sort_by_cell(ens.handle, grid, sp), 3)
+                for kind, ms_k in (("random", ms_sort), ("presorted", ms_pre)):
+                    print(json.dumps({"exp": "sort_by_cell", "precision": prec_name,
+                                      "input": kind, "n": a.n, "cells": g ** 3, "ms": ms_k,
+                                      "ns_per_particle": ms_k * 1e6 / a.n}), flush=True)
             for steps in (1, a.steps):
                 ms = timed(lambda: lb.boris_push(ens.handle, grid, w.dt, steps, sp), 5)
                 print(json.dumps({"exp": "grid_push", "precision": prec_name, "order": order,
