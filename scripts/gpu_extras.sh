@@ -25,21 +25,27 @@ if [ $what = pic ] || [ $what = all ]; then
   echo pic rc=$?
 fi
 if [ $what = ncu ] || [ $what = all ]; then
-  run() {  # name case kernel-regex skip
-    timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"$3" -s $4 -c 1 \
-      -o gpurun_out/prof2/$1 -f python scripts/prof_kernels.py --case $2 > gpurun_out/prof2/$1.log 2>&1
-    echo "ncu $1 rc=$?"
+  cap() {  # name kernel-regex skip command...
+    local name=$1 rx=$2 skip=$3; shift 3
+    timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c 1 \
+      -o gpurun_out/prof2/$name -f "$@" > gpurun_out/prof2/$name.log 2>&1
+    echo "ncu $name rc=$?"
   }
-  run aos32 aos32 k_stream_aos 1
-  run aos64 aos64 k_stream_aos 1
-  run soa64 soa64 k_stream_soa_vec 1
-  run fusedarr fusedarr k_fused_arrays 1
-  run grid grid '^k_fused$' 1
-  run deposit deposit k_deposit 1
-  run rs_scatter sort k_rs_scatter 0
-  timeout 600 $NCU --set full --clock-control none --import-source on -k regex:'^k_fused$' -s 1 -c 1 \
-    -o gpurun_out/prof2/fused_planewave_fp32 -f python scripts/prof_fused.py > gpurun_out/prof2/fused_pw.log 2>&1
-  echo "ncu fused_planewave rc=$?"
+  PK="python scripts/prof_kernels.py --case"
+  PF="python scripts/prof_fused.py"
+  cap aos32 k_stream_aos 1 $PK aos32
+  cap aos64 k_stream_aos 1 $PK aos64
+  cap soa64 k_stream_soa_vec 1 $PK soa64
+  cap fusedarr k_fused_arrays 1 $PK fusedarr
+  cap grid '^k_stream_soa_grid' 1 $PK grid
+  cap deposit '^k_deposit_runs' 1 $PK deposit
+  cap rs_scatter k_rs_scatter 0 $PK sort
+  cap permute_soa k_permute_soa 0 $PK sort
+  cap fused_planewave_fp32 '^k_fused$' 1 $PF
+  cap fused_planewave_fp64 '^k_fused$' 1 $PF --precision fp64
+  cap fused_mdipole_fp32 '^k_fused$' 1 $PF --field mdipole
+  cap fused_mdipole_fp64 '^k_fused$' 1 $PF --field mdipole --precision fp64
+  cap fused_uniform_C3_fp64 '^k_fused$' 1 $PF --field uniform --precision fp64
 fi
 if [ $what = sanitize ] || [ $what = all ]; then
   for tool in memcheck racecheck synccheck initcheck; do

@@ -17,6 +17,7 @@ METRICS = [
     ("issue_%", "smsp__issue_active.avg.pct_of_peak_sustained_active", 1, None),
     ("fma_pipe_%", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", 1, None),
     ("fp64_pipe_%", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", 1, None),
+    ("alu_pipe_%", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", 1, None),
     ("xu_pipe_%", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", 1, None),
     ("lsu_pipe_%", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", 1, None),
     ("l1_hit_%", "l1tex__t_sector_hit_rate.pct", 1, None),

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Launch one fused analytic push (for ncu): C4 plane wave (default) or m-dipole.
+"""Launch one fused analytic push (for ncu): C4 plane wave (default), m-dipole, or the
+C3 crossed uniform field.
 
-    python scripts/prof_fused.py [--field plane_wave|mdipole] [--precision fp32|fp64]
+    python scripts/prof_fused.py [--field plane_wave|mdipole|uniform] [--precision fp32|fp64]
                                  [--n 10000000] [--steps 100] [--reps 3]
 """
 import argparse
@@ -27,7 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
-    w = synth.config("C4", n=a.n)
+    w = synth.config("C3" if a.field == "uniform" else "C4", n=a.n)
     prec = lb.BORIS_FP32 if a.precision == "fp32" else lb.BORIS_FP64
     ens = SoaEnsemble(a.n, prec, w.types, w.light_velocity, with_fields=False)
     ens.fill(w.generate(0, a.n, device="cuda"))
@@ -36,6 +37,8 @@ def main():
         pw = w.plane_wave
         f = lb.boris_field_create_plane_wave(pw["E0"], pw["k_hat"], pw["e_hat"], pw["omega"],
                                              pw["k"], pw["phase0"])
+    elif a.field == "uniform":
+        f = lb.boris_field_create_uniform(w.uniform_E, w.uniform_B)
     else:
         k = synth.OMEGA0 / synth.C_LIGHT
         f = lb.boris_field_create_mdipole(k * math.sqrt(3e21 / synth.C_LIGHT), synth.OMEGA0, k)

@@ -812,6 +812,65 @@ def test_deposit_current_vs_oracle(precision, layout):
     ens.close()
 
 
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("mode", ["sorted", "one_cell", "few_cells", "tiny"])
+def test_deposit_current_runs_and_contention(precision, mode, layout):
+    """The run-accumulating SoA deposition on the inputs it is built for: particles
+    sorted by cell (long runs, lanes' open cells merged by the warp segmented scan),
+    every particle in one cell (maximum contention), a 2x2x2 block of cells (runs
+    broken at every few particles), and n < one warp.  Bound: summation error
+    <= tol x sum over particles of |q w v| / cell volume (a dropped or doubled particle
+    is ~1/n of that sum, far above tol)."""
+    h, params, _, _ = grid_setup(precision)
+    w = synth.config("C5")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    n = 19 if mode == "tiny" else N_SMALL
+    d = w.generate(0, n)
+    org, sp = np.array(params[:3]), np.array(params[3:6])
+    if mode in ("one_cell", "few_cells"):
+        g = torch.Generator().manual_seed(5)
+        span = 1 if mode == "one_cell" else 2
+        cell = torch.randint(0, span, (n, 3), generator=g).double() + 5.0
+        frac = 0.1 + 0.8 * torch.rand((n, 3), generator=g, dtype=torch.float64)
+        pos = torch.from_numpy(org) + (cell + frac) * torch.from_numpy(sp)
+        d["x"], d["y"], d["z"] = pos[:, 0].clone(), pos[:, 1].clone(), pos[:, 2].clone()
+    d = rounded(d, precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    ens = cls(n, PREC[precision], w.types, w.light_velocity, with_fields=False)
+    ens.fill(d)
+    ens.wrap()
+    if mode == "sorted":
+        lb.boris_ensemble_sort_by_cell(ens.handle, h)
+        torch.cuda.synchronize()
+        s = ens.state()
+        d = {k: s[k] for k in ("x", "y", "z", "px", "py", "pz", "weight", "type")}
+    nx, ny, nz = int(params[6]), int(params[7]), int(params[8])
+    dt_ = torch.float32 if precision == "fp32" else torch.float64
+    J = [torch.zeros((nz, ny, nx), dtype=dt_, device="cuda") for _ in range(3)]
+    lb.boris_deposit_current(ens.handle, h, w.dt, *(j.data_ptr() for j in J))
+    torch.cuda.synchronize()
+    Jg = torch.stack(J).double().cpu().numpy()
+    pos, mom = stack3(d, "x", "y", "z"), stack3(d, "px", "py", "pz")
+    typ = d["type"].numpy().astype(np.int64)
+    tq = np.array([t[0] for t in w.types])
+    tm = np.array([t[1] for t in w.types])
+    Jr = oracle.deposit_current(pos, mom, d["weight"].numpy(), typ, list(tq), list(tm),
+                                w.light_velocity, w.dt, params)
+    m = tm[typ][:, None]
+    gam = np.sqrt(1.0 + ((mom / (m * w.light_velocity)) ** 2).sum(1))[:, None]
+    vol = params[3] * params[4] * params[5]
+    contrib = (np.abs(tq[typ])[:, None] * d["weight"].numpy()[:, None]
+               * np.abs(mom / (m * gam))).sum(0) / vol
+    tol = 1e-5 if precision == "fp32" else 1e-12
+    err = np.abs(Jg - Jr).reshape(3, -1).max(1)
+    assert (err <= tol * contrib).all(), (err / contrib, mode)
+    assert np.abs(Jr).max() > 1e3 * tol * contrib.max()     # the check is not vacuous
+    lb.boris_field_destroy(h)
+    ens.close()
+
+
 # ---------------------------------------------------------------------------
 # Alternative pushers (SURVEY §8(f) row 4; readings c-vay, c-hc).
 # ---------------------------------------------------------------------------
