@@ -861,12 +861,14 @@ def test_deposit_current_runs_and_contention(precision, mode, layout):
     m = tm[typ][:, None]
     gam = np.sqrt(1.0 + ((mom / (m * w.light_velocity)) ** 2).sum(1))[:, None]
     vol = params[3] * params[4] * params[5]
-    contrib = (np.abs(tq[typ])[:, None] * d["weight"].numpy()[:, None]
-               * np.abs(mom / (m * gam))).sum(0) / vol
+    single = (np.abs(tq[typ])[:, None] * d["weight"].numpy()[:, None]
+              * np.abs(mom / (m * gam))) / vol
+    contrib = single.sum(0)
     tol = 1e-5 if precision == "fp32" else 1e-12
     err = np.abs(Jg - Jr).reshape(3, -1).max(1)
     assert (err <= tol * contrib).all(), (err / contrib, mode)
-    assert np.abs(Jr).max() > 1e3 * tol * contrib.max()     # the check is not vacuous
+    # not vacuous: a typical single particle's current is above the bound
+    assert (np.median(single, 0) > 4 * tol * contrib).all()
     lb.boris_field_destroy(h)
     ens.close()
 
