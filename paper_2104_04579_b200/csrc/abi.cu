@@ -321,6 +321,15 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
     } else if (f->kind == FK_GRID) {
         a.grid = make_grid_args<FP>(f);
     }
+    // exact zeros off the y (E) and z (B) axes -> the YZ fused specialisation;
+    // BORIS_FUSED_GENERIC=1 (read per push) forces the generic kernel (tests)
+    const char *gen = getenv("BORIS_FUSED_GENERIC");
+    const bool allow = !(gen && gen[0] == '1');
+    if (allow && f->kind == FK_UNIFORM)
+        a.yz = a.E[0] == 0 && a.E[2] == 0 && a.B[0] == 0 && a.B[1] == 0;
+    else if (allow && f->kind == FK_PLANE_WAVE)
+        a.yz = a.cE[0] == 0 && a.cE[2] == 0 && a.cB[0] == 0 && a.cB[1] == 0 &&
+               a.kf[1] == 0 && a.kf[2] == 0 && a.kvec[1] == 0 && a.kvec[2] == 0;
     return a;
 }
 

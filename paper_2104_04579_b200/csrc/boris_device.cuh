@@ -152,6 +152,30 @@ __device__ __forceinline__ FP boris_momentum_dir(FP &ux, FP &uy, FP &uz, FP c, c
     return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
 }
 
+// boris_momentum_dir for the axis-aligned orientation E = c aE_y y^, B = c ab_z z^
+// (a plane wave with k^ = x^, e^ = y^, or a uniform E || y^, B || z^; either may
+// be zero).  It performs exactly the roundings boris_momentum_dir performs when
+// ae = (0, aey, 0) and ab = (0, 0, abz) — every product with an exact zero and
+// every addition of a signed zero drops out — so results are bitwise identical
+// (up to the sign of zero components) with ~40 % fewer instructions per step.
+template <typename FP, bool UNIT>
+__device__ __forceinline__ FP boris_momentum_yz(FP &ux, FP &uy, FP &uz, FP c, FP aey, FP abz,
+                                                FP kappa2, FP &gamma) {
+    const FP ey = UNIT ? aey : b_mul(c, aey);
+    uy = b_add(uy, ey);
+    const FP inv_gn = b_rsqrt(b_fma(kappa2, b_norm2(ux, uy, uz), FP(1)));
+    const FP ta = UNIT ? inv_gn : b_mul(inv_gn, c);
+    const FP tz = b_mul(ta, abz);
+    // boris_rotate with t = (0, 0, tz): s = (0, 0, sf tz)
+    const FP sz = b_mul(b_mul(FP(2), b_rcpx(b_add(FP(1), b_mul(tz, tz)))), tz);
+    const FP upx = b_add(ux, b_mul(uy, tz));
+    const FP upy = b_add(uy, -b_mul(ux, tz));
+    ux = b_add(ux, b_mul(upy, sz));
+    uy = b_add(uy, -b_mul(upx, sz));
+    uy = b_add(uy, ey);
+    return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
+}
+
 // One Boris momentum update on the scaled momentum u (steps a4-a9).
 // Returns 1/gamma^{n+1/2}; writes gamma^{n+1/2} to `gamma`.
 template <typename FP>

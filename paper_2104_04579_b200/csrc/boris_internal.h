@@ -51,6 +51,9 @@ struct AnalyticArgs {
     double w0t0, w0dt;
     // grid (FK_GRID): CIC gather of packed node records (grid.cuh)
     GridArgs<FP> grid;
+    // uniform / plane wave with E || y^, B || z^ (k^ = x^): the k_fused YZ
+    // specialisation applies (boris_momentum_yz; bitwise identical results)
+    int yz;
 };
 
 // Per-launch description of an ensemble's storage.

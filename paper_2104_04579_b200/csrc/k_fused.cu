@@ -213,7 +213,7 @@ constexpr int kFlush = 8;
 // Launches are split into chunks of kTimeTab steps on the host.
 constexpr int kTimeTab = 1024;
 
-template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER>
+template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER, bool YZ>
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
@@ -262,17 +262,25 @@ __global__ void __launch_bounds__(kFusedThreads)
             auto step = [&](int j) {
                 FP inv_g;
                 if constexpr (FIELD == FK_UNIFORM) {
-                    if constexpr (PUSHER == PUSHER_BORIS)
+                    if constexpr (YZ)
+                        inv_g = boris_momentum_yz<FP, true>(ux, uy, uz, FP(1), ae[1], ab[2],
+                                                            tc.kappa2, gam);
+                    else if constexpr (PUSHER == PUSHER_BORIS)
                         inv_g = boris_momentum_dir<FP, true>(ux, uy, uz, FP(1), ae, ab, tc.kappa2,
                                                              gam);
                     else
                         inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, fa.E[0], fa.E[1], fa.E[2],
                                                             fa.B[0], fa.B[1], fa.B[2], tc, gam);
                 } else if constexpr (FIELD == FK_PLANE_WAVE) {
-                    const FP phi = b_fma(fa.kf[0], dx, b_fma(fa.kf[1], dy, b_fma(fa.kf[2], dz,
-                                   b_fma(-(FP)j, fa.wdtf, phia))));
+                    // YZ: kf = (kf0, 0, 0) exactly, the dropped fma terms add signed zeros
+                    const FP phi = YZ ? b_fma(fa.kf[0], dx, b_fma(-(FP)j, fa.wdtf, phia))
+                                      : b_fma(fa.kf[0], dx, b_fma(fa.kf[1], dy, b_fma(fa.kf[2], dz,
+                                        b_fma(-(FP)j, fa.wdtf, phia))));
                     const FP c = cos_small(phi);  // E = E0 e_hat c, B = E0 (k_hat x e_hat) c
-                    if constexpr (PUSHER == PUSHER_BORIS)
+                    if constexpr (YZ)
+                        inv_g = boris_momentum_yz<FP, false>(ux, uy, uz, c, ae[1], ab[2],
+                                                             tc.kappa2, gam);
+                    else if constexpr (PUSHER == PUSHER_BORIS)
                         inv_g = boris_momentum_dir<FP, false>(ux, uy, uz, c, ae, ab, tc.kappa2,
                                                               gam);
                     else
@@ -341,8 +349,16 @@ static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
     const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER><<<(unsigned)grid, kFusedThreads, 0, st>>>(
-        e, fa, co, n_steps, diag ? diag->partials : nullptr);
+    constexpr bool kHasYZ =
+        (FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE) && PUSHER == PUSHER_BORIS;
+    if (kHasYZ && fa.yz)
+        k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, kHasYZ>
+            <<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, co, n_steps,
+                                                       diag ? diag->partials : nullptr);
+    else
+        k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, false>
+            <<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, co, n_steps,
+                                                       diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }

@@ -123,11 +123,12 @@ def fused(name, cfg, layout, precision, n, steps, iters=5, field_kind=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--fused-only", action="store_true")
     a = ap.parse_args()
     n1 = 10_000_000 if a.quick else 100_000_000
     three = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
     rows = []
-    for n in ([10_000_000] + ([n1] if n1 != 10_000_000 else [])):
+    for n in ([] if a.fused_only else [10_000_000] + ([n1] if n1 != 10_000_000 else [])):
         for layout in ("soa", "aos"):
             for prec in ("fp32", "fp64"):
                 rows.append(streaming(f"C2-{layout}-{prec}", layout, prec, n))
@@ -137,6 +138,12 @@ def main():
     rows.append(fused("C3-aos-fp64-crossed-100", "C3", "aos", "fp64", 10_000_000, 100))
     rows.append(fused("C4-soa-fp32-planewave-100", "C4", "soa", "fp32", n1, 100))
     rows.append(fused("C4-soa-fp64-planewave-100", "C4", "soa", "fp64", n1 // 4, 100))
+    # the same two C4 rows and C3 through the generic (any-orientation) fused kernel
+    os.environ["BORIS_FUSED_GENERIC"] = "1"
+    rows.append(fused("C3-aos-fp64-crossed-100-generic", "C3", "aos", "fp64", 10_000_000, 100))
+    rows.append(fused("C4-soa-fp32-planewave-100-generic", "C4", "soa", "fp32", n1, 100))
+    rows.append(fused("C4-soa-fp64-planewave-100-generic", "C4", "soa", "fp64", n1 // 4, 100))
+    del os.environ["BORIS_FUSED_GENERIC"]
     rows.append(fused("mdipole-soa-fp32-100", "C4", "soa", "fp32", n1 // 4, 100,
                       field_kind="mdipole"))
     rows.append(fused("mdipole-soa-fp64-100", "C4", "soa", "fp64", n1 // 10, 100,

@@ -297,6 +297,45 @@ def test_C4_plane_wave_parity(precision, layout):
     print(precision, layout, worst)
 
 
+@pytest.mark.parametrize("orient", ["k=z,e=x", "oblique"])
+def test_plane_wave_other_orientations_parity(orient):
+    """Orientations other than k = x, e = y take the generic fused kernel."""
+    w = synth.config("C4")
+    if orient == "k=z,e=x":
+        w.plane_wave.update(k_hat=(0.0, 0.0, 1.0), e_hat=(1.0, 0.0, 0.0))
+    else:
+        k = np.array([1.0, 2.0, 2.0]) / 3.0
+        e = np.array([2.0, 1.0, -2.0]) / 3.0          # orthogonal to k
+        w.plane_wave.update(k_hat=tuple(k), e_hat=tuple(e))
+    run_parity(w, "soa", "fp32", N_SMALL, checks=(1, 10, 100))
+    run_parity(w, "soa", "fp64", N_SMALL, checks=(1, 10, 100))
+
+
+@pytest.mark.parametrize("cfg,layout,precision", [("C4", "soa", "fp32"), ("C4", "aos", "fp64"),
+                                                  ("C3", "aos", "fp64"), ("C3", "soa", "fp32"),
+                                                  ("C1", "soa", "fp64")])
+def test_axis_aligned_specialisation_equals_generic_bitwise(cfg, layout, precision, monkeypatch):
+    """k_fused's YZ specialisation (E || y, B || z: C1, C3, C4) drops only products with
+    exact zeros, so it equals the generic kernel bitwise (BORIS_FUSED_GENERIC=1)."""
+    w = synth.config(cfg)
+    n = w.n if cfg == "C1" else N_SMALL
+    steps = 37
+    states = []
+    for generic in ("0", "1"):
+        monkeypatch.setenv("BORIS_FUSED_GENERIC", generic)
+        _, ens, f = build(w, layout, precision, n)
+        diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+        lb.boris_push_diag(ens.handle, f, w.dt, steps, diag.data_ptr())
+        torch.cuda.synchronize()
+        states.append((ens.state(), diag.cpu()))
+        lb.boris_field_destroy(f)
+        ens.close()
+    (a, da), (b, db) = states
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(da, db)
+
+
 def mdipole_workload():
     # m-dipole at P = 0.1 PW (PAPER.md L396-426, reading c12: A0 = k sqrt(3P/c)).
     w = synth.config("C4")
