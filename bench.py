@@ -116,9 +116,9 @@ def cpu_baseline(workload, target_s=15.0, sample=1 << 21, threads=None):
             workload.light_velocity, oracle.FIELD_ARRAYS)
     oracle.push(*args, E=E, B=B, dt=workload.dt, n_steps=1, n_threads=threads)  # warm-up
     t0 = time.perf_counter()
-    oracle.push(*args, E=E, B=B, dt=workload.dt, n_steps=1, n_threads=threads)
-    t1 = time.perf_counter() - t0
-    steps = int(max(1, min(2000, target_s / max(t1, 1e-6))))
+    oracle.push(*args, E=E, B=B, dt=workload.dt, n_steps=8, n_threads=threads)
+    t1 = (time.perf_counter() - t0) / 8          # steady per-step time (calibration)
+    steps = int(max(1, min(4000, target_s / max(t1, 1e-6))))
     t0 = time.perf_counter()
     oracle.push(*args, E=E, B=B, dt=workload.dt, n_steps=steps, n_threads=threads)
     el = time.perf_counter() - t0

@@ -257,6 +257,9 @@ boris_status boris_field_destroy(boris_field *field);
  * keep their relative order), so the result is deterministic.  Per-particle
  * field arrays are NOT permuted (they belong to the caller).  Device ensembles,
  * n < 2^32.  Asynchronous (temporary buffers are stream-ordered allocations).
+ * Scratch: 16 B + (SoA) 8 FP + 2 B, or (AoS) one record, per particle, taken from
+ * a library-owned per-device memory pool that keeps up to 1/16 of the device
+ * memory mapped between calls (repeated sorts do not re-map their scratch).
  */
 boris_status boris_ensemble_sort_by_cell(boris_ensemble *ens, const boris_field *grid,
                                          void *stream);
