@@ -106,10 +106,24 @@ __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
         g2 = s2;
         f3 = j0 - j1x;
     } else {
-        FP sn, cs;
-        if constexpr (sizeof(FP) == 4) sincosf(xi, &sn, &cs);
-        else sincos(xi, &sn, &cs);
-        const FP ix = FP(1) / xi, ix2 = ix * ix, ix3 = ix2 * ix;
+        FP sn, cs, ix;
+        if constexpr (sizeof(FP) == 4) {
+#ifdef BORIS_PRECISE_MATH
+            sincosf(xi, &sn, &cs);
+            ix = 1.0f / xi;
+#else
+            // fp32 Cody-Waite reduction to [-pi, pi], then MUFU sin/cos (abs error
+            // ~2^-21, the fp32 rounding of xi itself) and rcp.approx
+            const float q = rintf(xi * 0.15915494f);
+            const float r = __fmaf_rn(-q, -1.7484555e-07f, __fmaf_rn(-q, 6.2831855f, xi));
+            __sincosf(r, &sn, &cs);
+            ix = b_rcpx(xi);
+#endif
+        } else {
+            sincos(xi, &sn, &cs);
+            ix = FP(1) / xi;
+        }
+        const FP ix2 = ix * ix, ix3 = ix2 * ix;
         const FP f1 = sn * ix2 - cs * ix;
         const FP f2 = (FP(3) * ix3 - ix) * sn - FP(3) * cs * ix2;
         f3 = (ix - ix3) * sn + cs * ix2;
