@@ -75,6 +75,9 @@ typedef struct boris_particle_type {
 } boris_particle_type;
 #define BORIS_MAX_TYPES 32
 
+/* Largest particle count of one ensemble handle (2^40). */
+#define BORIS_MAX_PARTICLES ((int64_t)1 << 40)
+
 /*
  * AoS record layouts (paper §3: "Particle { FP3 position; FP3
  * momentum; FP weight; FP gamma; short type; }", 34 B -> 36 B aligned in
@@ -108,7 +111,8 @@ const char *boris_last_error(void);
  * types 0, gamma 1, weight 1, time 0).  SoA arrays are 256 B aligned and padded
  * to a multiple of 8 particles; padding is never downloaded or counted.
  * `types[0..n_types)` is copied.  n == 0 is allowed.
- * Errors: INVALID_ARG (n < 0, n_types not in [1, BORIS_MAX_TYPES], mass <= 0,
+ * Errors: INVALID_ARG (n outside [0, BORIS_MAX_PARTICLES] — also for the wrap
+ * functions —, n_types not in [1, BORIS_MAX_TYPES], mass <= 0,
  * non-finite values, light_velocity <= 0), NO_DEVICE, OUT_OF_MEMORY, CUDA.
  */
 boris_status boris_ensemble_create(int32_t device, boris_layout layout,

@@ -53,11 +53,13 @@ def _stale(target, deps):
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> str:
-    """Build libboris.so, or with `tag` a variant build/libboris_<tag>.so compiled with
+    """Build libboris.so, or with `tag` a variant tuning_libs/libboris_<tag>.so (outside
+    the gpurun-ignored build/ directory, so it travels to the GPU box) compiled with
     extra -D `defines` (tuning experiments; the product is always libboris.so)."""
     srcs = sources()
     hdrs = headers()
-    lib = LIB if not tag else os.path.join(BUILD_DIR, f"libboris_{tag}.so")
+    lib = LIB if not tag else os.path.join(PKG, "tuning_libs", f"libboris_{tag}.so")
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     if not force and not _stale(lib, srcs + hdrs + [__file__]):
         return lib
     os.makedirs(BUILD_DIR, exist_ok=True)

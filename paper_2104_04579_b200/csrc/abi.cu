@@ -587,7 +587,8 @@ boris_status boris_ensemble_create(int32_t device, boris_layout layout, boris_pr
         return fail(BORIS_E_INVALID_ARG, "bad layout %d", layout);
     if (precision != BORIS_FP32 && precision != BORIS_FP64)
         return fail(BORIS_E_INVALID_ARG, "bad precision %d", precision);
-    if (n < 0) return fail(BORIS_E_INVALID_ARG, "n < 0");
+    if (n < 0 || n > BORIS_MAX_PARTICLES)
+        return fail(BORIS_E_INVALID_ARG, "n = %lld outside [0, 2^40]", (long long)n);
     boris_status s = check_types_table(types, n_types, light_velocity);
     if (s != BORIS_OK) return s;
     if ((s = check_device(device)) != BORIS_OK) return s;
@@ -644,7 +645,8 @@ boris_status boris_ensemble_wrap_soa(int32_t device, int32_t memory, boris_preci
         return fail(BORIS_E_INVALID_ARG, "bad precision %d", precision);
     if (memory != BORIS_MEMORY_DEVICE && memory != BORIS_MEMORY_HOST)
         return fail(BORIS_E_INVALID_ARG, "bad memory kind %d", memory);
-    if (n < 0) return fail(BORIS_E_INVALID_ARG, "n < 0");
+    if (n < 0 || n > BORIS_MAX_PARTICLES)
+        return fail(BORIS_E_INVALID_ARG, "n = %lld outside [0, 2^40]", (long long)n);
     if (n > 0 && (!x || !y || !z || !px || !py || !pz || !gamma))
         return fail(BORIS_E_INVALID_ARG, "x, y, z, px, py, pz and gamma must be non-NULL");
     boris_status s = check_types_table(types, n_types, light_velocity);
@@ -679,7 +681,8 @@ boris_status boris_ensemble_wrap_aos(int32_t device, int32_t memory, boris_preci
         return fail(BORIS_E_INVALID_ARG, "bad precision %d", precision);
     if (memory != BORIS_MEMORY_DEVICE && memory != BORIS_MEMORY_HOST)
         return fail(BORIS_E_INVALID_ARG, "bad memory kind %d", memory);
-    if (n < 0) return fail(BORIS_E_INVALID_ARG, "n < 0");
+    if (n < 0 || n > BORIS_MAX_PARTICLES)
+        return fail(BORIS_E_INVALID_ARG, "n = %lld outside [0, 2^40]", (long long)n);
     if (n > 0 && !records) return fail(BORIS_E_INVALID_ARG, "records is NULL");
     if (((uintptr_t)records & 15u) != 0)
         return fail(BORIS_E_INVALID_ARG, "AoS records must be 16 B aligned");

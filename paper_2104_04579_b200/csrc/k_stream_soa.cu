@@ -108,8 +108,16 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
 // PIC case: the grid field changes between steps, so pushes are single steps).
 // Same 128-bit state streaming as k_stream_soa_vec; the V particles of a thread
 // gather their 8 nodes each with independent loads (ILP hides the L1/L2 latency).
+// 3 resident blocks per SM (<= 80 registers): the gathers are latency-bound, so
+// occupancy wins over per-thread registers (measured, 10^7 sorted, 64^3 grid:
+// fp32 14.8 -> 12.3 ps, fp64 29.4 -> 23.7 ps vs the unconstrained ~100-register
+// build; 4 blocks spill and lose again; profiles/r01/exp_grid_minblocks.txt).
+#ifndef BORIS_GRID_MINB
+#define BORIS_GRID_MINB 3
+#endif
+#define BORIS_GRID_BOUNDS __launch_bounds__(kStreamThreads, BORIS_GRID_MINB)
 template <typename FP, bool MULTI, bool DIAG>
-__global__ void __launch_bounds__(kStreamThreads)
+__global__ void BORIS_GRID_BOUNDS
     k_stream_soa_grid(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
                       const __grid_constant__ Coefs<FP> co, int64_t n_groups, int64_t n,
                       double *partials) {

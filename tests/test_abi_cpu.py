@@ -103,6 +103,10 @@ def test_argument_validation_host_only(lb):
     with pytest.raises(lb.BorisError) as ei:
         lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP32, -1, [(1.0, 1.0)], 1.0)
     assert ei.value.status == lb.BORIS_E_INVALID_ARG
+    with pytest.raises(lb.BorisError) as ei:   # beyond BORIS_MAX_PARTICLES
+        lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP64,
+                                 lb.BORIS_MAX_PARTICLES + 1, [(1.0, 1.0)], 1.0)
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
     with pytest.raises(lb.BorisError) as ei:   # mass must be > 0
         lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP32, 1, [(1.0, 0.0)], 1.0)
     assert ei.value.status == lb.BORIS_E_INVALID_ARG

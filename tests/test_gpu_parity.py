@@ -582,6 +582,18 @@ def test_edge_cases_and_errors():
         bad.wrap()
 
 
+def test_out_of_memory_is_reported_and_not_sticky():
+    """An ensemble larger than the device (2^40 fp64 SoA particles = 72 TB) fails with
+    OUT_OF_MEMORY, leaves no sticky CUDA error, and the library keeps working."""
+    with pytest.raises(lb.BorisError) as ei:
+        lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP64, lb.BORIS_MAX_PARTICLES,
+                                 [synth.ELECTRON], synth.C_LIGHT)
+    assert ei.value.status == lb.BORIS_E_OUT_OF_MEMORY
+    w = synth.config("C2")
+    run_parity(w, "soa", "fp32", 4099, checks=(1, 2))
+    torch.cuda.synchronize()
+
+
 # ---------------------------------------------------------------------------
 # Full BASELINE sizes, in the launch configuration bench.py times: sampled parity.
 # ---------------------------------------------------------------------------
