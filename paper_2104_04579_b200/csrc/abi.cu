@@ -400,6 +400,12 @@ int64_t host_chunk_particles() {
     return v / 8 * 8;
 }
 
+static boris_status build_pipeline(const boris_ensemble *e, bool with_fields, HostPipeline *p);
+
+// The staging pipeline of a host-resident ensemble, created on first use (and
+// re-created with field staging when a per-particle-field push first needs it;
+// the old one may still be in use by enqueued work, hence the device sync).
+// On failure nothing is left half-built.
 boris_status ensure_pipeline(boris_ensemble *e, bool with_fields) {
     if (e->pipe && (e->pipe->with_fields || !with_fields)) return BORIS_OK;
     if (e->pipe) {
@@ -408,7 +414,16 @@ boris_status ensure_pipeline(boris_ensemble *e, bool with_fields) {
         e->pipe = nullptr;
     }
     HostPipeline *p = new HostPipeline();
+    const boris_status s = build_pipeline(e, with_fields, p);
+    if (s != BORIS_OK) {
+        free_pipeline(p);
+        return s;
+    }
     e->pipe = p;
+    return BORIS_OK;
+}
+
+static boris_status build_pipeline(const boris_ensemble *e, bool with_fields, HostPipeline *p) {
     p->with_fields = with_fields;
     p->chunk = host_chunk_particles();
     if (p->chunk > e->n) p->chunk = (e->n + 7) / 8 * 8;
