@@ -431,33 +431,81 @@ static bool deposit_runs_enabled() {
     return v == 1;
 }
 
-template <typename FP>
-__global__ void __launch_bounds__(DepRuns<FP>::WARPS * 32)
+// DIRECT (fp32, 16 B aligned arrays): no shared-memory staging; each lane loads
+// its K = 8 consecutive particles with two 128-bit loads per array (a warp's
+// loads cover the tile contiguously) and keeps them in registers.
+// BORIS_DEPOSIT_STAGING=smem keeps the shared-memory staged kernel for fp32 too.
+static bool deposit_direct_enabled() {
+    const char *s = getenv("BORIS_DEPOSIT_STAGING");
+    return !(s && s[0] == 's');
+}
+
+#ifndef BORIS_DEP_DIRECT_MINB
+#define BORIS_DEP_DIRECT_MINB 2
+#endif
+template <typename FP, bool DIRECT>
+__global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
+                                  DIRECT ? BORIS_DEP_DIRECT_MINB : 6)
     k_deposit_runs(EnsView e, const __grid_constant__ GridArgs<FP> g,
                    const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz) {
     using R = DepRuns<FP>;
-    __shared__ FP s[R::WARPS][7][R::SK];
-    __shared__ int16_t s_ty[R::WARPS][R::SK];
+    constexpr int NW = DIRECT ? 8 : R::WARPS;
+    __shared__ FP s[DIRECT ? 1 : R::WARPS][7][DIRECT ? 1 : R::SK];
+    __shared__ int16_t s_ty[DIRECT ? 1 : R::WARPS][DIRECT ? 1 : R::SK];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const FP *arr[7] = {(const FP *)e.soa.x, (const FP *)e.soa.y, (const FP *)e.soa.z,
                         (const FP *)e.soa.px, (const FP *)e.soa.py, (const FP *)e.soa.pz,
                         (const FP *)e.soa.w};
     const bool multi = dc.n_types > 1 && e.soa.type;
-    const int64_t stride = (int64_t)gridDim.x * R::WARPS * R::TILE;
-    for (int64_t base = ((int64_t)blockIdx.x * R::WARPS + warp) * R::TILE; base < e.n;
+    const int64_t stride = (int64_t)gridDim.x * NW * R::TILE;
+    FP rv[DIRECT ? 7 : 1][DIRECT ? R::K : 1];
+    int16_t rty[DIRECT ? R::K : 1];
+    for (int64_t base = ((int64_t)blockIdx.x * NW + warp) * R::TILE; base < e.n;
          base += stride) {
-        // coalesced warp loads into the skewed tile
+        if constexpr (DIRECT) {
+            static_assert(sizeof(FP) == 4 && R::K == 8, "direct staging: fp32, K = 8");
+            const int64_t i0 = base + lane * R::K;
+            if (i0 + R::K <= e.n) {
 #pragma unroll
-        for (int r = 0; r < R::K; ++r) {
-            const int p = r * 32 + lane;
-            const int64_t i = base + p;
-            const int sp = p + p / R::K;
+                for (int a = 0; a < 7; ++a)
 #pragma unroll
-            for (int a = 0; a < 7; ++a)
-                s[warp][a][sp] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
-            if (multi) s_ty[warp][sp] = (i < e.n) ? e.soa.type[i] : (int16_t)0;
+                    for (int h = 0; h < 2; ++h) {
+                        float4 v = arr[a] ? __ldg(reinterpret_cast<const float4 *>(arr[a] + i0) + h)
+                                          : make_float4(1.f, 1.f, 1.f, 1.f);
+                        rv[a][4 * h] = v.x; rv[a][4 * h + 1] = v.y;
+                        rv[a][4 * h + 2] = v.z; rv[a][4 * h + 3] = v.w;
+                    }
+                if (multi) {
+                    const uint4 t4 = __ldg(reinterpret_cast<const uint4 *>(e.soa.type + i0));
+                    const uint32_t tw[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                    for (int j = 0; j < R::K; ++j)
+                        rty[j] = (int16_t)(tw[j >> 1] >> (16 * (j & 1)));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < R::K; ++j) {
+                    const int64_t i = i0 + j;
+#pragma unroll
+                    for (int a = 0; a < 7; ++a)
+                        rv[a][j] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
+                    rty[j] = (multi && i < e.n) ? e.soa.type[i] : (int16_t)0;
+                }
+            }
+        } else {
+            // coalesced warp loads into the skewed tile
+#pragma unroll
+            for (int r = 0; r < R::K; ++r) {
+                const int p = r * 32 + lane;
+                const int64_t i = base + p;
+                const int sp = p + p / R::K;
+#pragma unroll
+                for (int a = 0; a < 7; ++a)
+                    s[warp][a][sp] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
+                if (multi) s_ty[warp][sp] = (i < e.n) ? e.soa.type[i] : (int16_t)0;
+            }
+            __syncwarp();
         }
-        __syncwarp();
         FP acc[8][3];
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
@@ -481,14 +529,20 @@ __global__ void __launch_bounds__(DepRuns<FP>::WARPS * 32)
                     }
                 }
         };
+        constexpr int kUnrollJ = DIRECT ? R::K : 1;  // register arrays need constant indices
+#pragma unroll kUnrollJ
         for (int j = 0; j < R::K; ++j) {
             const int p = lane * R::K + j;
             if (base + p >= e.n) break;
-            const int sp = p + p / R::K;
-            const FP x = s[warp][0][sp], y = s[warp][1][sp], z = s[warp][2][sp];
-            const FP px = s[warp][3][sp], py = s[warp][4][sp], pz = s[warp][5][sp];
-            const FP w = s[warp][6][sp];
-            const DepCoef<FP> t = dc.t[multi ? s_ty[warp][sp] : 0];
+            const int sp = DIRECT ? 0 : p + p / R::K;
+            const FP x = DIRECT ? rv[0][j] : s[warp][0][sp];
+            const FP y = DIRECT ? rv[1][j] : s[warp][1][sp];
+            const FP z = DIRECT ? rv[2][j] : s[warp][2][sp];
+            const FP px = DIRECT ? rv[3][j] : s[warp][3][sp];
+            const FP py = DIRECT ? rv[4][j] : s[warp][4][sp];
+            const FP pz = DIRECT ? rv[5][j] : s[warp][5][sp];
+            const FP w = DIRECT ? rv[6][j] : s[warp][6][sp];
+            const DepCoef<FP> t = dc.t[multi ? (DIRECT ? rty[j] : s_ty[warp][sp]) : 0];
             const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
             const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
             const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
@@ -565,10 +619,24 @@ cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoe
     if (e.layout == BORIS_LAYOUT_SOA && deposit_runs_enabled()) {
         using R = DepRuns<FP>;
         const int64_t tiles = (e.n + R::TILE - 1) / R::TILE;
+        auto al16 = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
+        const bool direct = sizeof(FP) == 4 && deposit_direct_enabled() && al16(e.soa.x) &&
+                            al16(e.soa.y) && al16(e.soa.z) && al16(e.soa.px) &&
+                            al16(e.soa.py) && al16(e.soa.pz) && al16(e.soa.w) &&
+                            al16(e.soa.type);
+        if constexpr (sizeof(FP) == 4) {
+            if (direct) {
+                const int64_t blocks = (tiles + 7) / 8;
+                const unsigned grid = (unsigned)stream_grid(blocks, 4, device);
+                k_deposit_runs<FP, true><<<grid, 8 * 32, 0, st>>>(e, g, dc, (FP *)Jx,
+                                                                   (FP *)Jy, (FP *)Jz);
+                return cudaGetLastError();
+            }
+        }
         const int64_t blocks = (tiles + R::WARPS - 1) / R::WARPS;
         const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
-        k_deposit_runs<FP><<<grid, R::WARPS * 32, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy,
-                                                            (FP *)Jz);
+        k_deposit_runs<FP, false><<<grid, R::WARPS * 32, 0, st>>>(e, g, dc, (FP *)Jx,
+                                                                   (FP *)Jy, (FP *)Jz);
         return cudaGetLastError();
     }
     const int64_t blocks = (e.n + 255) / 256;
