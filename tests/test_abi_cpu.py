@@ -179,3 +179,15 @@ def test_oracle_and_cuda_path_share_nothing():
             assert not re.search(r"#include\s+[\"<](libboris|boris_device|boris_internal)", txt), fn
             assert not re.search(r"^\s*(import|from)\s+(paper_2104_04579_b200|synth)\b", txt,
                                  re.M), fn
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libboris.so every call raises ImportError."""
+    import subprocess
+    import sys
+    env = dict(os.environ, LIBBORIS_PATH=str(tmp_path / "absent" / "libboris.so"))
+    r = subprocess.run([sys.executable, "-c",
+                        "import paper_2104_04579_b200 as lb; lb.boris_abi_version()"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "no CPU fallback" in r.stderr
