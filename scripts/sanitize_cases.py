@@ -100,6 +100,7 @@ def main():
                 e.wrap()
                 lb.boris_ensemble_sort_by_cell(e.handle, grid)
                 lb.boris_push_diag(e.handle, grid, w.dt, 3, dp)
+                lb.boris_push_diag(e.handle, grid, w.dt, 1, dp)   # streaming grid step
                 lb.boris_deposit_current(e.handle, grid, w.dt, *(j.data_ptr() for j in J))
                 lb.boris_field_evaluate(grid, e.handle, 0.0, e.field)
                 for flags in (lb.BORIS_PUSH_PUSHER_VAY, lb.BORIS_PUSH_PUSHER_HIGUERA_CARY):
@@ -108,6 +109,13 @@ def main():
                     f = analytic("plane_wave")
                     lb.boris_push_ex(e.handle, f, w.dt, 2, flags, dp)
                     lb.boris_field_destroy(f)
+                for generic in ("0", "1"):   # axis-aligned specialisation and generic
+                    os.environ["BORIS_FUSED_GENERIC"] = generic
+                    for kind in ("uniform", "plane_wave"):
+                        f = analytic(kind)
+                        lb.boris_push_diag(e.handle, f, w.dt, 11, dp)
+                        lb.boris_field_destroy(f)
+                os.environ.pop("BORIS_FUSED_GENERIC")
                 torch.cuda.synchronize()
                 e.close()
         lb.boris_field_destroy(grid)
