@@ -35,6 +35,10 @@ boris_status ok() {
     return BORIS_OK;
 }
 boris_status cuda_fail(cudaError_t err, const char *what) {
+    // The error is reported here, so take it out of the runtime's per-thread
+    // last-error slot: a failed cudaMalloc (not sticky) would otherwise surface
+    // again at the next launch check and fail an unrelated push.
+    (void)cudaGetLastError();
     if (err == cudaErrorMemoryAllocation)
         return fail(BORIS_E_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(err));
     return fail(BORIS_E_CUDA, "%s: %s", what, cudaGetErrorString(err));

@@ -102,18 +102,21 @@ __device__ __forceinline__ FP b_cross(FP a, FP b, FP c, FP d) {
     return b_fma(a, b, -b_mul(c, d));
 }
 
-// Steps a6 (s from t, eq. 13) and a7 (rotation, eq. 12) given t.
+// Steps a6 (s from t, eq. 13) and a7 (rotation, eq. 12) given t.  Each cross
+// product component is folded into the addition as two nested FMAs,
+// u'_x = fma(u_y, t_z, fma(-u_z, t_y, u_x)), so a zero component of t (the
+// axis-aligned fields) drops out exactly: fma(-u_z, 0, u_x) == u_x.
 template <typename FP>
 __device__ __forceinline__ void boris_rotate(FP &ux, FP &uy, FP &uz, FP tx, FP ty, FP tz) {
-    const FP sf = b_mul(FP(2), b_rcpx(b_add(FP(1), b_norm2(tx, ty, tz))));
+    const FP sf = b_mul(FP(2), b_rcpx(b_fma(tx, tx, b_fma(ty, ty, b_fma(tz, tz, FP(1))))));
     const FP sx = b_mul(sf, tx), sy = b_mul(sf, ty), sz = b_mul(sf, tz);
     // u' = u^- + u^- x t ; u^+ = u^- + u' x s
-    const FP upx = b_add(ux, b_cross(uy, tz, uz, ty));
-    const FP upy = b_add(uy, b_cross(uz, tx, ux, tz));
-    const FP upz = b_add(uz, b_cross(ux, ty, uy, tx));
-    ux = b_add(ux, b_cross(upy, sz, upz, sy));
-    uy = b_add(uy, b_cross(upz, sx, upx, sz));
-    uz = b_add(uz, b_cross(upx, sy, upy, sx));
+    const FP upx = b_fma(uy, tz, b_fma(-uz, ty, ux));
+    const FP upy = b_fma(uz, tx, b_fma(-ux, tz, uy));
+    const FP upz = b_fma(ux, ty, b_fma(-uy, tx, uz));
+    ux = b_fma(upy, sz, b_fma(-upz, sy, ux));
+    uy = b_fma(upz, sx, b_fma(-upx, sz, uy));
+    uz = b_fma(upx, sy, b_fma(-upy, sx, uz));
 }
 
 // Step a9: gamma^{n+1/2} (eq. 5, reading c3); returns its reciprocal.
@@ -137,18 +140,17 @@ __device__ __forceinline__ FP boris_gamma(FP ux, FP uy, FP uz, FP kappa2, FP &ga
 template <typename FP, bool UNIT>
 __device__ __forceinline__ FP boris_momentum_dir(FP &ux, FP &uy, FP &uz, FP c, const FP (&ae)[3],
                                                  const FP (&ab)[3], FP kappa2, FP &gamma) {
-    const FP ex = UNIT ? ae[0] : b_mul(c, ae[0]);
-    const FP ey = UNIT ? ae[1] : b_mul(c, ae[1]);
-    const FP ez = UNIT ? ae[2] : b_mul(c, ae[2]);
-    ux = b_add(ux, ex);
-    uy = b_add(uy, ey);
-    uz = b_add(uz, ez);
+    // half kicks: u + c aE e as one FMA (UNIT: c = 1, a plain addition)
+    auto kick = [&](FP u, FP a) { return UNIT ? b_add(u, a) : b_fma(c, a, u); };
+    ux = kick(ux, ae[0]);
+    uy = kick(uy, ae[1]);
+    uz = kick(uz, ae[2]);
     const FP inv_gn = b_rsqrt(b_fma(kappa2, b_norm2(ux, uy, uz), FP(1)));
     const FP ta = UNIT ? inv_gn : b_mul(inv_gn, c);
     boris_rotate<FP>(ux, uy, uz, b_mul(ta, ab[0]), b_mul(ta, ab[1]), b_mul(ta, ab[2]));
-    ux = b_add(ux, ex);
-    uy = b_add(uy, ey);
-    uz = b_add(uz, ez);
+    ux = kick(ux, ae[0]);
+    uy = kick(uy, ae[1]);
+    uz = kick(uz, ae[2]);
     return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
 }
 
@@ -161,18 +163,17 @@ __device__ __forceinline__ FP boris_momentum_dir(FP &ux, FP &uy, FP &uz, FP c, c
 template <typename FP, bool UNIT>
 __device__ __forceinline__ FP boris_momentum_yz(FP &ux, FP &uy, FP &uz, FP c, FP aey, FP abz,
                                                 FP kappa2, FP &gamma) {
-    const FP ey = UNIT ? aey : b_mul(c, aey);
-    uy = b_add(uy, ey);
+    uy = UNIT ? b_add(uy, aey) : b_fma(c, aey, uy);
     const FP inv_gn = b_rsqrt(b_fma(kappa2, b_norm2(ux, uy, uz), FP(1)));
     const FP ta = UNIT ? inv_gn : b_mul(inv_gn, c);
     const FP tz = b_mul(ta, abz);
     // boris_rotate with t = (0, 0, tz): s = (0, 0, sf tz)
-    const FP sz = b_mul(b_mul(FP(2), b_rcpx(b_add(FP(1), b_mul(tz, tz)))), tz);
-    const FP upx = b_add(ux, b_mul(uy, tz));
-    const FP upy = b_add(uy, -b_mul(ux, tz));
-    ux = b_add(ux, b_mul(upy, sz));
-    uy = b_add(uy, -b_mul(upx, sz));
-    uy = b_add(uy, ey);
+    const FP sz = b_mul(b_mul(FP(2), b_rcpx(b_fma(tz, tz, FP(1)))), tz);
+    const FP upx = b_fma(uy, tz, ux);
+    const FP upy = b_fma(-ux, tz, uy);
+    ux = b_fma(upy, sz, ux);
+    uy = b_fma(-upx, sz, uy);
+    uy = UNIT ? b_add(uy, aey) : b_fma(c, aey, uy);
     return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
 }
 
@@ -181,11 +182,10 @@ __device__ __forceinline__ FP boris_momentum_yz(FP &ux, FP &uy, FP &uz, FP c, FP
 template <typename FP>
 __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP Ey, FP Ez, FP Bx,
                                              FP By, FP Bz, const TypeCoef<FP> &tc, FP &gamma) {
-    // a4: first electric half kick (eq. 9)
-    const FP ex = b_mul(tc.aE, Ex), ey = b_mul(tc.aE, Ey), ez = b_mul(tc.aE, Ez);
-    ux = b_add(ux, ex);
-    uy = b_add(uy, ey);
-    uz = b_add(uz, ez);
+    // a4: first electric half kick (eq. 9), u + aE E as one FMA per component
+    ux = b_fma(tc.aE, Ex, ux);
+    uy = b_fma(tc.aE, Ey, uy);
+    uz = b_fma(tc.aE, Ez, uz);
     // a5: 1/gamma_n, gamma_n = gamma(u^-) (L162, reading c2)
     const FP inv_gn = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
     // a6: rotation vectors (eq. 13)
@@ -193,9 +193,9 @@ __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP E
     // a6-a7: s and the rotation (eq. 12-13)
     boris_rotate<FP>(ux, uy, uz, b_mul(ta, Bx), b_mul(ta, By), b_mul(ta, Bz));
     // a8: second electric half kick (eq. 10)
-    ux = b_add(ux, ex);
-    uy = b_add(uy, ey);
-    uz = b_add(uz, ez);
+    ux = b_fma(tc.aE, Ex, ux);
+    uy = b_fma(tc.aE, Ey, uy);
+    uz = b_fma(tc.aE, Ez, uz);
     // a9: gamma^{n+1/2} (eq. 5, reading c3) and its reciprocal
     return boris_gamma<FP>(ux, uy, uz, tc.kappa2, gamma);
 }

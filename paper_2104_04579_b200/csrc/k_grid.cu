@@ -440,8 +440,11 @@ static bool deposit_direct_enabled() {
     return !(s && s[0] == 's');
 }
 
+#ifndef BORIS_DEP_PREFETCH
+#define BORIS_DEP_PREFETCH 0
+#endif
 #ifndef BORIS_DEP_DIRECT_MINB
-#define BORIS_DEP_DIRECT_MINB 2
+#define BORIS_DEP_DIRECT_MINB (BORIS_DEP_PREFETCH ? 1 : 2)
 #endif
 template <typename FP, bool DIRECT>
 __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
@@ -460,11 +463,13 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
     const int64_t stride = (int64_t)gridDim.x * NW * R::TILE;
     FP rv[DIRECT ? 7 : 1][DIRECT ? R::K : 1];
     int16_t rty[DIRECT ? R::K : 1];
-    for (int64_t base = ((int64_t)blockIdx.x * NW + warp) * R::TILE; base < e.n;
-         base += stride) {
+    // DIRECT: lane's K = 8 consecutive particles of the tile at `tb`, two 128-bit
+    // loads per array (scalar loads in the ragged last tile).
+    auto load_direct = [&](int64_t tb, FP (&dv)[DIRECT ? 7 : 1][DIRECT ? R::K : 1],
+                           int16_t (&dty)[DIRECT ? R::K : 1]) {
         if constexpr (DIRECT) {
             static_assert(sizeof(FP) == 4 && R::K == 8, "direct staging: fp32, K = 8");
-            const int64_t i0 = base + lane * R::K;
+            const int64_t i0 = tb + lane * R::K;
             if (i0 + R::K <= e.n) {
 #pragma unroll
                 for (int a = 0; a < 7; ++a)
@@ -472,15 +477,15 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
                     for (int h = 0; h < 2; ++h) {
                         float4 v = arr[a] ? __ldg(reinterpret_cast<const float4 *>(arr[a] + i0) + h)
                                           : make_float4(1.f, 1.f, 1.f, 1.f);
-                        rv[a][4 * h] = v.x; rv[a][4 * h + 1] = v.y;
-                        rv[a][4 * h + 2] = v.z; rv[a][4 * h + 3] = v.w;
+                        dv[a][4 * h] = v.x; dv[a][4 * h + 1] = v.y;
+                        dv[a][4 * h + 2] = v.z; dv[a][4 * h + 3] = v.w;
                     }
                 if (multi) {
                     const uint4 t4 = __ldg(reinterpret_cast<const uint4 *>(e.soa.type + i0));
                     const uint32_t tw[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
                     for (int j = 0; j < R::K; ++j)
-                        rty[j] = (int16_t)(tw[j >> 1] >> (16 * (j & 1)));
+                        dty[j] = (int16_t)(tw[j >> 1] >> (16 * (j & 1)));
                 }
             } else {
 #pragma unroll
@@ -488,10 +493,34 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
                     const int64_t i = i0 + j;
 #pragma unroll
                     for (int a = 0; a < 7; ++a)
-                        rv[a][j] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
-                    rty[j] = (multi && i < e.n) ? e.soa.type[i] : (int16_t)0;
+                        dv[a][j] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
+                    dty[j] = (multi && i < e.n) ? e.soa.type[i] : (int16_t)0;
                 }
             }
+        }
+    };
+#if BORIS_DEP_PREFETCH
+    // software pipeline: the next tile's loads are in flight during this tile's
+    // arithmetic, scan and atomics
+    FP nv[DIRECT ? 7 : 1][DIRECT ? R::K : 1];
+    int16_t nty[DIRECT ? R::K : 1];
+    const int64_t first = ((int64_t)blockIdx.x * NW + warp) * R::TILE;
+    if (DIRECT && first < e.n) load_direct(first, nv, nty);
+#endif
+    for (int64_t base = ((int64_t)blockIdx.x * NW + warp) * R::TILE; base < e.n;
+         base += stride) {
+        if constexpr (DIRECT) {
+#if BORIS_DEP_PREFETCH
+#pragma unroll
+            for (int j = 0; j < R::K; ++j) {
+#pragma unroll
+                for (int a = 0; a < 7; ++a) rv[a][j] = nv[a][j];
+                rty[j] = nty[j];
+            }
+            if (base + stride < e.n) load_direct(base + stride, nv, nty);
+#else
+            load_direct(base, rv, rty);
+#endif
         } else {
             // coalesced warp loads into the skewed tile
 #pragma unroll
