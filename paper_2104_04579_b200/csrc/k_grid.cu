@@ -619,8 +619,11 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
             const uint32_t next = __shfl_down_sync(full, key, 1);
             const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
             const int seg = 31 - __clz(heads & (full >> (31 - lane)));
+            // only as many scan rounds as the longest segment needs (warp-uniform)
+            const int span = (int)__reduce_max_sync(full, (unsigned)(lane - seg));
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
+                if (off > span) break;
                 const bool take = lane - off >= seg;
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
@@ -638,12 +641,23 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
 }
 
 template <typename FP>
+__global__ void k_zero3(FP *a, FP *b, FP *c, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        a[i] = FP(0);
+        b[i] = FP(0);
+        c[i] = FP(0);
+    }
+}
+
+template <typename FP>
 cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
                            void *Jx, void *Jy, void *Jz, int device, cudaStream_t st) {
     const int64_t ncell = (int64_t)g.n[0] * g.n[1] * g.n[2];
-    cudaError_t err = cudaMemsetAsync(Jx, 0, (size_t)ncell * sizeof(FP), st);
-    if (err == cudaSuccess) err = cudaMemsetAsync(Jy, 0, (size_t)ncell * sizeof(FP), st);
-    if (err == cudaSuccess) err = cudaMemsetAsync(Jz, 0, (size_t)ncell * sizeof(FP), st);
+    // zero J: one launch for the three arrays (three memsets cost ~3 launch gaps)
+    k_zero3<FP><<<(unsigned)((ncell + 255) / 256 < 4096 ? (ncell + 255) / 256 : 4096), 256, 0,
+                  st>>>((FP *)Jx, (FP *)Jy, (FP *)Jz, ncell);
+    cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess || e.n == 0) return err;
     if (e.layout == BORIS_LAYOUT_SOA && deposit_runs_enabled()) {
         using R = DepRuns<FP>;

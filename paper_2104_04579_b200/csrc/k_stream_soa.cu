@@ -205,6 +205,18 @@ static cudaError_t dispatch_soa_grid(const EnsView &e, const GridArgs<FP> &g,
 
 static bool aligned16(const void *p);
 
+// Grid single-step kernel: "tma" (k_stream_soa_grid_tma, state staged by bulk
+// copies) or "ldg" (k_stream_soa_grid); BORIS_GRID_KERNEL overrides the default.
+// Both are bitwise identical.
+static bool use_tma_grid() {
+    static int v = -1;
+    if (v < 0) {
+        const char *s = getenv("BORIS_GRID_KERNEL");
+        v = (s && s[0] == 't') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 // Returns cudaErrorNotSupported when the arrays are not 16 B aligned (the caller
 // then uses the fused kernel).
 template <typename FP>
@@ -220,6 +232,8 @@ cudaError_t launch_stream_soa_grid(const EnsView &e, const GridArgs<FP> &g, cons
                     aligned16(e.soa.g) && (!diag || !e.soa.w || aligned16(e.soa.w)) &&
                     (!multi || ((uintptr_t)e.soa.type & (2 * V - 1)) == 0);
     if (!al) return cudaErrorNotSupported;
+    if (use_tma_grid() && (!multi || aligned16(e.soa.type)))
+        return launch_stream_soa_grid_tma<FP>(e, g, co, multi, diag, device, st);
     const bool d = diag != nullptr;
     if (multi)
         return d ? dispatch_soa_grid<FP, true, true>(e, g, co, diag, device, st)
