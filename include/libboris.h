@@ -240,8 +240,9 @@ boris_status boris_field_create_mdipole(double A0, double omega0, double k, bori
  * Cartesian grid, node (i,j,k) at origin + (i, j, k) * spacing, gathered at each
  * particle's position r^n every step with the CIC (trilinear) form factor.
  * Ex..Bz: DEVICE arrays of nx*ny*nz FP on `device`, node (i,j,k) at
- * (k*ny + j)*nx + i; they are copied (packed into 8-FP node records owned by
- * the handle), so they may be freed after this call returns (synchronous).
+ * (k*ny + j)*nx + i; they are copied (packed into 12-FP x-pair records, node i
+ * and its periodic +x neighbour, owned by the handle: 12 FP per node of device
+ * memory), so they may be freed after this call returns (synchronous).
  * Errors: INVALID_ARG (n < 1, > 2^31 nodes, spacing <= 0, NULL), NO_DEVICE, CUDA.
  * Ensembles pushed with it must have the same precision and device (MISMATCH).
  */

@@ -1093,13 +1093,13 @@ boris_status boris_field_create_grid(int32_t device, boris_precision precision, 
         f->org[d] = origin[d];
         f->h[d] = spacing[d];
     }
-    cudaError_t err = cudaMalloc(&f->nodes, (size_t)ncell * 8 * fp_size(precision));
+    cudaError_t err = cudaMalloc(&f->nodes, (size_t)ncell * kGridRecord * fp_size(precision));
     if (err != cudaSuccess) {
         delete f;
         return cuda_fail(err, "cudaMalloc(grid nodes)");
     }
     const void *comps[6] = {Ex, Ey, Ez, Bx, By, Bz};
-    err = launch_grid_pack(precision, ncell, comps, f->nodes, 0);
+    err = launch_grid_pack(precision, ncell, nx, comps, f->nodes, 0);
     if (err == cudaSuccess) err = cudaDeviceSynchronize();
     if (err != cudaSuccess) {
         cudaFree(f->nodes);

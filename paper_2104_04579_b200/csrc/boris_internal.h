@@ -112,7 +112,7 @@ cudaError_t launch_fused(const EnsView &e, int field_kind, const AnalyticArgs<FP
 // Grid field support (k_grid.cu): pack 6 component arrays (ncell FP each) into
 // 8-FP node records; stable sort of an ensemble by grid cell (LSD radix sort of
 // (cell, index) pairs + permutation of every particle array).
-cudaError_t launch_grid_pack(int precision, int64_t ncell, const void *const comps[6],
+cudaError_t launch_grid_pack(int precision, int64_t ncell, int nx, const void *const comps[6],
                              void *nodes, cudaStream_t st);
 template <typename FP>
 cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int device, cudaStream_t st);

@@ -3,17 +3,19 @@
 // L72-79, L89-91: "each particle interacts with a set of nearby grid values of
 // the electromagnetic field, depending on the form factor"; reading c-grid in
 // DESIGN.md).  Node (i,j,k) sits at origin + (i hx, j hy, k hz); the grid repeats
-// with period (nx hx, ny hy, nz hz).  Nodes are packed as 8-FP records
-// (Ex Ey Ez Bx | By Bz 0 0): two 128-bit loads per node in fp32, four in fp64.
+// with period (nx hx, ny hy, nz hz).  Nodes are packed as x-pair records of
+// kGridRecord = 12 FP: node i followed by its periodic +x neighbour.
 #pragma once
 
 #include "boris_device.cuh"
 
 namespace boris {
 
+constexpr int kGridRecord = 12;  // FP per x-pair record: [E B](i) [E B](i+1)
+
 template <typename FP>
 struct GridArgs {
-    const FP *nodes;  // 8 FP per node, node (i,j,k) at (k*ny + j)*nx + i
+    const FP *nodes;  // x-pair records (12 FP), record (i,j,k) at (k*ny + j)*nx + i
     FP org[3];        // origin
     FP inv_h[3];      // 1 / spacing
     FP nf[3];         // n as FP
@@ -48,15 +50,24 @@ __device__ __forceinline__ uint32_t grid_cell(const GridArgs<FP> &g, FP x, FP y,
     return ((uint32_t)k0 * (uint32_t)g.n[1] + (uint32_t)j0) * (uint32_t)g.n[0] + (uint32_t)i0;
 }
 
-__device__ __forceinline__ void load_node(const float *nodes, uint32_t node, float (&e)[6]) {
-    const float4 a = __ldg(reinterpret_cast<const float4 *>(nodes) + 2 * (size_t)node);
-    const float4 b = __ldg(reinterpret_cast<const float4 *>(nodes) + 2 * (size_t)node + 1);
+// The two x-nodes (i0, i0+1 mod nx) of a cell row: one x-pair record, 12 FP,
+// e[0..5] = [E B](i0), e[6..11] = [E B](i0+1): three 128-bit loads in fp32, six
+// in fp64.  (The gathers are bound by L1 requests, 16 per particle with one
+// 8-FP record per node; 12 with pair records.)
+__device__ __forceinline__ void load_pair(const float *nodes, uint32_t rec, float (&e)[12]) {
+    const float4 *p = reinterpret_cast<const float4 *>(nodes) + 3 * (size_t)rec;
+    const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
     e[0] = a.x; e[1] = a.y; e[2] = a.z; e[3] = a.w; e[4] = b.x; e[5] = b.y;
+    e[6] = b.z; e[7] = b.w; e[8] = c.x; e[9] = c.y; e[10] = c.z; e[11] = c.w;
 }
-__device__ __forceinline__ void load_node(const double *nodes, uint32_t node, double (&e)[6]) {
-    const double2 *p = reinterpret_cast<const double2 *>(nodes) + 4 * (size_t)node;
-    const double2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-    e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y; e[4] = c.x; e[5] = c.y;
+__device__ __forceinline__ void load_pair(const double *nodes, uint32_t rec, double (&e)[12]) {
+    const double2 *p = reinterpret_cast<const double2 *>(nodes) + 6 * (size_t)rec;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const double2 v = __ldg(p + k);
+        e[2 * k] = v.x;
+        e[2 * k + 1] = v.y;
+    }
 }
 
 // E, B at (x, y, z): sum over the 8 nodes of the cell of wx wy wz F_node.
@@ -79,13 +90,13 @@ __device__ __forceinline__ void grid_gather(const GridArgs<FP> &g, FP x, FP y, F
             const FP wyz = b_mul(wy[b], wz[c]);
             const uint32_t row = ((uint32_t)iz[c] * (uint32_t)g.n[1] + (uint32_t)iy[b]) *
                                  (uint32_t)g.n[0];
+            FP pair[12];
+            load_pair(g.nodes, row + (uint32_t)ix[0], pair);
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
                 const FP wt = b_mul(wx[a], wyz);
-                FP node[6];
-                load_node(g.nodes, row + (uint32_t)ix[a], node);
 #pragma unroll
-                for (int q = 0; q < 6; ++q) acc[q] = b_fma(wt, node[q], acc[q]);
+                for (int q = 0; q < 6; ++q) acc[q] = b_fma(wt, pair[6 * a + q], acc[q]);
             }
         }
     Ex = acc[0]; Ey = acc[1]; Ez = acc[2];

@@ -9,22 +9,29 @@
 // cell keep their relative order => the result is deterministic.
 #include <vector>
 
+#include <type_traits>
+
 #include "boris_internal.h"
 
 namespace boris {
 
 // ---------------------------------------------------------------------------
-// Node packing: comps[c][node] -> nodes[8*node + {0,1,2,3,4,5}], pads zeroed.
+// Node packing into x-pair records: record i holds node i and its +x neighbour
+// (periodic), 12 FP = [E B](i) [E B](i+1): the CIC gather loads a cell's two
+// x-nodes with 3 (fp32) / 6 (fp64) 128-bit loads, 12 per particle instead of 16.
 // ---------------------------------------------------------------------------
 template <typename FP>
-__global__ void k_grid_pack(int64_t ncell, const FP *Ex, const FP *Ey, const FP *Ez,
+__global__ void k_grid_pack(int64_t ncell, int nx, const FP *Ex, const FP *Ey, const FP *Ez,
                             const FP *Bx, const FP *By, const FP *Bz, FP *nodes) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell; i += stride) {
-        FP *r = nodes + 8 * i;
-        r[0] = Ex[i]; r[1] = Ey[i]; r[2] = Ez[i];
-        r[3] = Bx[i]; r[4] = By[i]; r[5] = Bz[i];
-        r[6] = FP(0); r[7] = FP(0);
+        const int64_t ix = i % nx;
+        const int64_t i1 = i - ix + (ix + 1 == nx ? 0 : ix + 1);
+        FP *r = nodes + kGridRecord * i;
+        r[0] = Ex[i];  r[1] = Ey[i];  r[2] = Ez[i];
+        r[3] = Bx[i];  r[4] = By[i];  r[5] = Bz[i];
+        r[6] = Ex[i1]; r[7] = Ey[i1]; r[8] = Ez[i1];
+        r[9] = Bx[i1]; r[10] = By[i1]; r[11] = Bz[i1];
     }
 }
 
@@ -34,104 +41,141 @@ static unsigned grid1d(int64_t n, int threads = 256) {
     return (unsigned)(b > 0 ? b : 1);
 }
 
-cudaError_t launch_grid_pack(int precision, int64_t ncell, const void *const c[6], void *nodes,
-                             cudaStream_t st) {
+cudaError_t launch_grid_pack(int precision, int64_t ncell, int nx, const void *const c[6],
+                             void *nodes, cudaStream_t st) {
     if (precision == BORIS_FP32)
         k_grid_pack<float><<<grid1d(ncell), 256, 0, st>>>(
-            ncell, (const float *)c[0], (const float *)c[1], (const float *)c[2],
+            ncell, nx, (const float *)c[0], (const float *)c[1], (const float *)c[2],
             (const float *)c[3], (const float *)c[4], (const float *)c[5], (float *)nodes);
     else
         k_grid_pack<double><<<grid1d(ncell), 256, 0, st>>>(
-            ncell, (const double *)c[0], (const double *)c[1], (const double *)c[2],
+            ncell, nx, (const double *)c[0], (const double *)c[1], (const double *)c[2],
             (const double *)c[3], (const double *)c[4], (const double *)c[5], (double *)nodes);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// Sort keys: the cell of each particle (grid_cell, the gather's own base node).
-// ---------------------------------------------------------------------------
-template <typename FP>
-__global__ void k_cell_keys(EnsView e, const __grid_constant__ GridArgs<FP> g, uint32_t *keys,
-                            uint32_t *vals) {
-    constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e.n; i += stride) {
-        FP x, y, z;
-        if (e.layout == BORIS_LAYOUT_SOA) {
-            x = ((const FP *)e.soa.x)[i];
-            y = ((const FP *)e.soa.y)[i];
-            z = ((const FP *)e.soa.z)[i];
-        } else {
-            const FP *r = (const FP *)((const unsigned char *)e.aos + i * RB);
-            x = r[0]; y = r[1]; z = r[2];
-        }
-        keys[i] = grid_cell<FP>(g, x, y, z);
-        vals[i] = (uint32_t)i;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// LSD radix sort, 8-bit digits.  Tile = 256 threads x 8 keys; in round r thread t
-// owns key tile0 + r*256 + t, so (round, thread) order is the original order.
+// Stable LSD radix sort of the particles' cell keys, digits of up to 10 bits
+// (a 64^3 grid's 18-bit keys take 2 passes of 9 bits).  Tile = 256 threads x 8
+// keys; in round r thread t owns key tile0 + r*256 + t, so (round, thread) order
+// is the original order and the per-tile ranking below keeps it (stable).
+// Pass 0 computes the keys from the positions (grid_cell, the gather's own base
+// node) while histogramming; its values are the implicit indices i; the last
+// pass writes only values (the permutation).
 // ---------------------------------------------------------------------------
 constexpr int kRsThreads = 256;
 constexpr int kRsItems = 8;
 constexpr int kRsTile = kRsThreads * kRsItems;
 constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsMaxBits = 10;
+constexpr int kRsMaxBins = 1 << kRsMaxBits;
 
+// Histogram of one digit per tile, written digit-major: hist[d * nb + tile].
+// KEYS: compute the key of particle i from its position and store it.
+template <typename FP, bool KEYS>
 __global__ void __launch_bounds__(kRsThreads)
-    k_rs_hist(const uint32_t *keys, int64_t n, int shift, uint32_t *hist, int64_t nb) {
-    __shared__ uint32_t cnt[256];
-    cnt[threadIdx.x] = 0;
+    k_rs_hist(EnsView e, const __grid_constant__ GridArgs<FP> g, uint32_t *keys, int64_t n,
+              int shift, int bins, uint32_t *hist, int64_t nb) {
+    constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
+    __shared__ uint32_t cnt[kRsMaxBins];
+    for (int b = threadIdx.x; b < bins; b += kRsThreads) cnt[b] = 0;
     __syncthreads();
+    const uint32_t mask = (uint32_t)bins - 1u;
     const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
 #pragma unroll
     for (int r = 0; r < kRsItems; ++r) {
         const int64_t i = t0 + r * kRsThreads + threadIdx.x;
-        if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 0xFFu], 1u);
+        int d = bins;  // out of range: not counted
+        if (i < n) {
+            uint32_t key;
+            if constexpr (KEYS) {
+                FP x, y, z;
+                if (e.layout == BORIS_LAYOUT_SOA) {
+                    x = ((const FP *)e.soa.x)[i];
+                    y = ((const FP *)e.soa.y)[i];
+                    z = ((const FP *)e.soa.z)[i];
+                } else {
+                    const FP *rr = (const FP *)((const unsigned char *)e.aos + i * RB);
+                    x = rr[0]; y = rr[1]; z = rr[2];
+                }
+                key = grid_cell<FP>(g, x, y, z);
+                keys[i] = key;
+            } else {
+                key = keys[i];
+            }
+            d = (int)((key >> shift) & mask);
+        }
+        // warp-aggregated: one shared atomic per distinct digit in the warp (sorted
+        // input puts a whole warp in one bin, where per-lane atomics serialise)
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d < bins && __popc(peers & lt) == 0) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
     }
     __syncthreads();
-    hist[(int64_t)threadIdx.x * nb + blockIdx.x] = cnt[threadIdx.x];  // digit-major
+    for (int b = threadIdx.x; b < bins; b += kRsThreads)
+        hist[(int64_t)b * nb + blockIdx.x] = cnt[b];
 }
 
+// Scatter one digit: keys_out may be null (last pass), vals_in null (pass 0: i).
+// Warp w of a tile owns the contiguous keys [w*256, (w+1)*256) of the tile, in 8
+// rounds of 32, so (warp, round, lane) order is the original order (stable).
+// Pass 1: per-warp digit counts (match_any leaders, warp-synchronous).  Pass 2:
+// per digit, an exclusive scan over the warps starting at the tile's global
+// offset.  Pass 3: every key goes to its warp's running position for its digit.
+// Three block barriers per tile.
 __global__ void __launch_bounds__(kRsThreads)
     k_rs_scatter(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
-                 uint32_t *vals_out, int64_t n, int shift, const uint32_t *offs, int64_t nb) {
-    __shared__ uint32_t base[256];
-    __shared__ uint32_t wcnt[kRsWarps][257];
+                 uint32_t *vals_out, int64_t n, int shift, int bins, const uint32_t *offs,
+                 int64_t nb) {
+    __shared__ uint32_t wc[kRsWarps][kRsMaxBins];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    base[threadIdx.x] = offs[(int64_t)threadIdx.x * nb + blockIdx.x];
-    for (int w = 0; w < kRsWarps; ++w) wcnt[w][threadIdx.x] = 0;
-    if (threadIdx.x < kRsWarps) wcnt[threadIdx.x][256] = 0;
+    for (int b = threadIdx.x; b < bins; b += kRsThreads)
+#pragma unroll
+        for (int w = 0; w < kRsWarps; ++w) wc[w][b] = 0;
     __syncthreads();
-    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+    const uint32_t mask = (uint32_t)bins - 1u;
+    const int64_t w0 = (int64_t)blockIdx.x * kRsTile + (int64_t)warp * (kRsItems * 32);
     const unsigned lt = (1u << lane) - 1u;
+    uint32_t key[kRsItems], val[kRsItems];
+    unsigned peers[kRsItems];
+    int dig[kRsItems];
+#pragma unroll
     for (int r = 0; r < kRsItems; ++r) {
-        const int64_t i = t0 + r * kRsThreads + threadIdx.x;
+        const int64_t i = w0 + r * 32 + lane;
         const bool valid = i < n;
-        const uint32_t key = valid ? keys_in[i] : 0u;
-        const uint32_t val = valid ? vals_in[i] : 0u;
-        const int d = valid ? (int)((key >> shift) & 0xFFu) : 256;  // 256: no-op bin
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const int rank = __popc(peers & lt);
-        if (rank == 0) wcnt[warp][d] = __popc(peers);
-        __syncthreads();
-        if (valid) {
-            uint32_t before = 0;
-            for (int w = 0; w < warp; ++w) before += wcnt[w][d];
-            const uint32_t pos = base[d] + before + (uint32_t)rank;
-            keys_out[pos] = key;
-            vals_out[pos] = val;
-        }
-        __syncthreads();
-        uint32_t tot = 0;
+        key[r] = valid ? keys_in[i] : 0u;
+        val[r] = valid ? (vals_in ? vals_in[i] : (uint32_t)i) : 0u;
+        dig[r] = valid ? (int)((key[r] >> shift) & mask) : bins;
+    }
+#pragma unroll
+    for (int r = 0; r < kRsItems; ++r) {
+        peers[r] = __match_any_sync(0xffffffffu, dig[r]);
+        if (dig[r] < bins && __popc(peers[r] & lt) == 0) wc[warp][dig[r]] += __popc(peers[r]);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < bins; b += kRsThreads) {
+        uint32_t run = offs[(int64_t)b * nb + blockIdx.x];
+#pragma unroll
         for (int w = 0; w < kRsWarps; ++w) {
-            tot += wcnt[w][threadIdx.x];
-            wcnt[w][threadIdx.x] = 0;
+            const uint32_t c = wc[w][b];
+            wc[w][b] = run;
+            run += c;
         }
-        base[threadIdx.x] += tot;
-        if (threadIdx.x < kRsWarps) wcnt[threadIdx.x][256] = 0;
-        __syncthreads();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRsItems; ++r) {
+        const int d = dig[r];
+        const int rank = __popc(peers[r] & lt);
+        if (d < bins) {
+            const uint32_t pos = wc[warp][d] + (uint32_t)rank;
+            if (keys_out) keys_out[pos] = key[r];
+            vals_out[pos] = val[r];
+        }
+        __syncwarp();
+        if (d < bins && rank == 0) wc[warp][d] += __popc(peers[r]);
+        __syncwarp();
     }
 }
 
@@ -214,18 +258,91 @@ __global__ void k_gather_bytes(const unsigned char *in, unsigned char *out, cons
 }
 
 // All SoA arrays at once: blk[a*fb + i] = arr_a[perm[i]] (perm read once per i).
+// Four particles per thread: one 128-bit perm load, four independent gathers per
+// array (more loads in flight), 128-bit stores into the 256 B-aligned slices.
 template <typename FP>
-__global__ void k_permute_soa(SoaPtrs s, const uint32_t *perm, int64_t n, unsigned char *blk,
-                              size_t fb) {
+__global__ void __launch_bounds__(256)
+    k_permute_soa(SoaPtrs s, const uint32_t *perm, int64_t n, unsigned char *blk, size_t fb) {
     const FP *src[8] = {(const FP *)s.x, (const FP *)s.y, (const FP *)s.z, (const FP *)s.px,
                         (const FP *)s.py, (const FP *)s.pz, (const FP *)s.w, (const FP *)s.g};
+    const int64_t ng = n / 4;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const int64_t j = perm[i];
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < ng; q += stride) {
+        const uint4 j4 = __ldg(reinterpret_cast<const uint4 *>(perm) + q);
+        const uint32_t j[4] = {j4.x, j4.y, j4.z, j4.w};
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            if (!src[a]) continue;
+            FP v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = src[a][j[k]];
+            FP *out = (FP *)(blk + a * fb) + 4 * q;
+            if constexpr (sizeof(FP) == 4) {
+                *reinterpret_cast<float4 *>(out) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+                reinterpret_cast<double2 *>(out)[0] = make_double2(v[0], v[1]);
+                reinterpret_cast<double2 *>(out)[1] = make_double2(v[2], v[3]);
+            }
+        }
+        if (s.type) {
+            int16_t t[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) t[k] = s.type[j[k]];
+            const uint2 tv = make_uint2((uint32_t)(uint16_t)t[0] | ((uint32_t)(uint16_t)t[1] << 16),
+                                        (uint32_t)(uint16_t)t[2] | ((uint32_t)(uint16_t)t[3] << 16));
+            *reinterpret_cast<uint2 *>((int16_t *)(blk + 8 * fb) + 4 * q) = tv;
+        }
+    }
+    // ragged tail (n mod 4)
+    const int64_t i = 4 * ng + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const int64_t jj = perm[i];
 #pragma unroll
         for (int a = 0; a < 8; ++a)
-            if (src[a]) ((FP *)(blk + a * fb))[i] = src[a][j];
-        if (s.type) ((int16_t *)(blk + 8 * fb))[i] = s.type[j];
+            if (src[a]) ((FP *)(blk + a * fb))[i] = src[a][jj];
+        if (s.type) ((int16_t *)(blk + 8 * fb))[i] = s.type[jj];
+    }
+}
+
+// Copy the permuted slices back into the ensemble's arrays: 128-bit accesses when
+// every destination is 16 B-aligned (owned ensembles, most torch tensors), all
+// slices of a 4-particle group loaded before any store (ILP); scalar otherwise.
+template <typename FP>
+__global__ void __launch_bounds__(256)
+    k_copy_back_soa(SoaPtrs s, int64_t n, const unsigned char *blk, size_t fb, bool vec) {
+    FP *dst[8] = {(FP *)s.x, (FP *)s.y, (FP *)s.z, (FP *)s.px,
+                  (FP *)s.py, (FP *)s.pz, (FP *)s.w, (FP *)s.g};
+    using V = typename std::conditional<sizeof(FP) == 4, float4, double2>::type;
+    constexpr int W = 16 / sizeof(FP);  // particles per 128-bit vector
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t done = 0;
+    if (vec) {
+        const int64_t ng = n / 8;  // groups of 8 particles: W-multiples for both FP
+        for (int64_t q = t0; q < ng; q += stride) {
+            V v[8][8 / W];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int h = 0; h < 8 / W; ++h)
+                    if (dst[a])
+                        v[a][h] = reinterpret_cast<const V *>(blk + a * fb)[q * (8 / W) + h];
+            uint4 tv;
+            if (s.type) tv = reinterpret_cast<const uint4 *>(blk + 8 * fb)[q];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int h = 0; h < 8 / W; ++h)
+                    if (dst[a]) reinterpret_cast<V *>(dst[a])[q * (8 / W) + h] = v[a][h];
+            if (s.type) reinterpret_cast<uint4 *>(s.type)[q] = tv;
+        }
+        done = 8 * ng;
+    }
+    for (int64_t i = done + t0; i < n; i += stride) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+            if (dst[a]) dst[a][i] = ((const FP *)(blk + a * fb))[i];
+        if (s.type) s.type[i] = ((const int16_t *)(blk + 8 * fb))[i];
     }
 }
 
@@ -248,27 +365,37 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     const uint64_t ncell = (uint64_t)g.n[0] * g.n[1] * g.n[2];
     int bits = 1;
     while (bits < 32 && (1ull << bits) < ncell) ++bits;
-    const int passes = (bits + 7) / 8;
+    const int passes = (bits + kRsMaxBits - 1) / kRsMaxBits;
+    const int dbits = (bits + passes - 1) / passes;  // <= kRsMaxBits
+    const int bins = 1 << dbits;
     const int64_t nb = (n + kRsTile - 1) / kRsTile;
     constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
     const size_t tmp_bytes = e.layout == BORIS_LAYOUT_SOA ? 0 : (size_t)n * RB;
     unsigned char *buf = nullptr;
-    const size_t kv = (size_t)n * sizeof(uint32_t);
-    const size_t hist_bytes = (size_t)256 * nb * sizeof(uint32_t);
+    const int64_t nn = (n + 63) / 64 * 64;  // 256 B-aligned key/value arrays
+    const size_t kv = (size_t)nn * sizeof(uint32_t);
+    const size_t hist_bytes = (size_t)bins * nb * sizeof(uint32_t);
     cudaError_t err = scratch_alloc((void **)&buf, 4 * kv + hist_bytes + tmp_bytes + 256, st);
     if (err != cudaSuccess) return err;
-    uint32_t *k0 = (uint32_t *)buf, *v0 = k0 + n, *k1 = v0 + n, *v1 = k1 + n;
-    uint32_t *hist = v1 + n;
-    unsigned char *tmp = (unsigned char *)(hist + 256 * nb);
+    uint32_t *k0 = (uint32_t *)buf, *v0 = k0 + nn, *k1 = v0 + nn, *v1 = k1 + nn;
+    uint32_t *hist = v1 + nn;
+    unsigned char *tmp = (unsigned char *)(hist + (size_t)bins * nb);
     tmp = (unsigned char *)(((uintptr_t)tmp + 255) & ~(uintptr_t)255);
 
-    k_cell_keys<FP><<<grid1d(n), 256, 0, st>>>(e, g, k0, v0);
-    err = cudaGetLastError();
     for (int p = 0; p < passes && err == cudaSuccess; ++p) {
-        k_rs_hist<<<(unsigned)nb, kRsThreads, 0, st>>>(k0, n, 8 * p, hist, nb);
+        const int shift = dbits * p;
+        if (p == 0)
+            k_rs_hist<FP, true><<<(unsigned)nb, kRsThreads, 0, st>>>(e, g, k0, n, shift, bins,
+                                                                   hist, nb);
+        else
+            k_rs_hist<FP, false><<<(unsigned)nb, kRsThreads, 0, st>>>(e, g, k0, n, shift, bins,
+                                                                    hist, nb);
         if ((err = cudaGetLastError()) != cudaSuccess) break;
-        if ((err = exclusive_scan(hist, 256 * nb, st)) != cudaSuccess) break;
-        k_rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(k0, v0, k1, v1, n, 8 * p, hist, nb);
+        if ((err = exclusive_scan(hist, (int64_t)bins * nb, st)) != cudaSuccess) break;
+        const bool last = p == passes - 1;
+        k_rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(k0, p == 0 ? nullptr : v0,
+                                                          last ? nullptr : k1, v1, n, shift,
+                                                          bins, hist, nb);
         err = cudaGetLastError();
         uint32_t *t;
         t = k0; k0 = k1; k1 = t;
@@ -282,17 +409,17 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
             const size_t fb = ((size_t)n * sizeof(FP) + 255) / 256 * 256;
             err = scratch_alloc((void **)&blk, 8 * fb + (size_t)n * 2 + 256, st);
             if (err == cudaSuccess) {
-                k_permute_soa<FP><<<grid1d(n), 256, 0, st>>>(e.soa, v0, n, blk, fb);
+                k_permute_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(e.soa, v0, n, blk, fb);
                 err = cudaGetLastError();
-                void *arrs[8] = {e.soa.x, e.soa.y, e.soa.z, e.soa.px,
-                                 e.soa.py, e.soa.pz, e.soa.w, e.soa.g};
-                for (int a = 0; a < 8 && err == cudaSuccess; ++a)
-                    if (arrs[a])
-                        err = cudaMemcpyAsync(arrs[a], blk + a * fb, (size_t)n * sizeof(FP),
-                                              cudaMemcpyDeviceToDevice, st);
-                if (err == cudaSuccess && e.soa.type)
-                    err = cudaMemcpyAsync(e.soa.type, blk + 8 * fb, (size_t)n * 2,
-                                          cudaMemcpyDeviceToDevice, st);
+                if (err == cudaSuccess) {  // one copy-back launch for all arrays
+                    auto al16 = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
+                    const bool vec = al16(e.soa.x) && al16(e.soa.y) && al16(e.soa.z) &&
+                                     al16(e.soa.px) && al16(e.soa.py) && al16(e.soa.pz) &&
+                                     al16(e.soa.w) && al16(e.soa.g) && al16(e.soa.type);
+                    k_copy_back_soa<FP><<<grid1d((n + 7) / 8), 256, 0, st>>>(e.soa, n, blk, fb,
+                                                                              vec);
+                    err = cudaGetLastError();
+                }
                 scratch_free(blk, st);
             }
         } else {

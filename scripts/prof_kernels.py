@@ -31,6 +31,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", required=True)
     ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--steps", type=int, default=1, help="grid case: steps per push")
     a = ap.parse_args()
     n = a.n
     w = synth.config("C2", n=n)
@@ -51,7 +52,7 @@ def main():
         lb.boris_ensemble_sort_by_cell(ens.handle, h, sp)
         if a.case == "grid":
             for _ in range(2):
-                lb.boris_push(ens.handle, h, w.dt, 1, sp)
+                lb.boris_push(ens.handle, h, w.dt, a.steps, sp)
         elif a.case == "deposit":
             J = [torch.zeros((64, 64, 64), device="cuda") for _ in range(3)]
             for _ in range(2):
