@@ -285,6 +285,23 @@ boris_status boris_deposit_current(const boris_ensemble *ens, const boris_field 
                                    void *Jx, void *Jy, void *Jz, void *stream);
 
 /*
+ * Fused PIC particle step (field interpolation to the particles,
+ * the push, and the current "computed and added to Maxwell's equations"): one
+ * push of size dt with the field gathered from `grid` (as boris_push(ens, grid,
+ * dt, 1, stream)) followed by the current deposition of the new state onto the
+ * same grid (as boris_deposit_current(ens, grid, dt, Jx, Jy, Jz, stream)), in one
+ * kernel for 16 B-aligned SoA ensembles (r, p and w are read once), else as the
+ * two launches.  The ensemble state is bitwise the push's; J (DEVICE, nx*ny*nz FP
+ * each, zeroed first) equals the separate deposition up to the order of its
+ * float atomics.  d_diag (DEVICE, 2 doubles, or NULL): {sum KE, N} after the step,
+ * as boris_push_diag.  The ensemble time advances by dt.  Errors: INVALID_ARG
+ * (NULL ens/grid/J, non-grid field, dt not finite), MISMATCH (precision or
+ * device), UNSUPPORTED (host-resident ensemble), CUDA.  Asynchronous.
+ */
+boris_status boris_push_deposit(boris_ensemble *ens, const boris_field *grid, double dt,
+                                void *Jx, void *Jy, void *Jz, double *d_diag, void *stream);
+
+/*
  * "Precalculated fields" (L369-371, reading c6): evaluate the analytic field
  * `analytic` (uniform / plane wave / m-dipole) at every particle's current
  * position r_i at time t and write it into the per-particle field `out` (arrays

@@ -55,6 +55,7 @@ EXPORTED = (
     "boris_ensemble_set_time", "boris_field_create_arrays_soa", "boris_field_create_arrays_aos",
     "boris_field_create_uniform", "boris_field_create_plane_wave", "boris_field_create_mdipole",
     "boris_field_create_grid", "boris_ensemble_sort_by_cell", "boris_deposit_current",
+    "boris_push_deposit",
     "boris_field_destroy", "boris_field_evaluate", "boris_push", "boris_push_diag", "boris_push_ex",
     "boris_kinetic_energy",
 )
@@ -103,6 +104,7 @@ _SIGNATURES = {
     "boris_field_create_grid": ([_i32, _i32, _i32, _i32, _i32, _dp, _dp] + [_vp] * 6 + [_hp], _i32),
     "boris_ensemble_sort_by_cell": ([_vp, _vp, _vp], _i32),
     "boris_deposit_current": ([_vp, _vp, _d, _vp, _vp, _vp, _vp], _i32),
+    "boris_push_deposit": ([_vp, _vp, _d, _vp, _vp, _vp, _vp, _vp], _i32),
     "boris_field_evaluate": ([_vp, _vp, _d, _vp, _vp], _i32),
     "boris_push": ([_vp, _vp, _d, _i64, _vp], _i32),
     "boris_push_diag": ([_vp, _vp, _d, _i64, _vp, _vp], _i32),
@@ -342,6 +344,12 @@ def boris_deposit_current(ens, grid, dt, Jx, Jy, Jz, stream=None):
     """CIC current deposition at the half-step position into device arrays Jx..Jz."""
     _check(load_library().boris_deposit_current(ens, grid, dt, Jx, Jy, Jz, _stream(stream)),
            "boris_deposit_current")
+
+
+def boris_push_deposit(ens, grid, dt, Jx, Jy, Jz, d_diag=None, stream=None):
+    """One grid-gather push followed by the current deposition of the new state (fused)."""
+    _check(load_library().boris_push_deposit(ens, grid, dt, Jx, Jy, Jz, d_diag, _stream(stream)),
+           "boris_push_deposit")
 
 
 def boris_field_destroy(field):

@@ -1130,6 +1130,27 @@ static DepCoefs<FP> make_dep_coefs(const boris_ensemble *e, const boris_field *g
     return dc;
 }
 
+template <typename FP>
+static cudaError_t push_deposit_view(boris_ensemble *e, const boris_field *grid, double dt,
+                                     void *Jx, void *Jy, void *Jz, DiagOut *dp, cudaStream_t st) {
+    const GridArgs<FP> g = make_grid_args<FP>(grid);
+    const DepCoefs<FP> dc = make_dep_coefs<FP>(e, grid, dt);
+    const EnsView v = e->view();
+    const int64_t ncell = (int64_t)grid->gn[0] * grid->gn[1] * grid->gn[2];
+    if (v.layout == BORIS_LAYOUT_SOA) {
+        cudaError_t err = launch_zero3<FP>(Jx, Jy, Jz, ncell, st);
+        if (err != cudaSuccess) return err;
+        err = launch_push_deposit_soa<FP>(v, g, make_coefs<FP>(e, dt), dc, Jx, Jy, Jz,
+                                          e->multi(), dp, e->device, st);
+        if (err != cudaErrorNotSupported) return err;
+    }
+    // AoS or unaligned: the push, then the deposition (which zeroes J)
+    cudaError_t err = push_view<FP>(e, v, grid, grid->soa, grid->aos, e->time, dt, 1,
+                                    BORIS_PUSH_AUTO, dp, st);
+    if (err != cudaSuccess) return err;
+    return launch_deposit<FP>(v, g, dc, Jx, Jy, Jz, e->device, st);
+}
+
 extern "C" {
 
 boris_status boris_deposit_current(const boris_ensemble *e, const boris_field *grid, double dt,
@@ -1152,6 +1173,33 @@ boris_status boris_deposit_current(const boris_ensemble *e, const boris_field *g
                                      make_dep_coefs<double>(e, grid, dt), Jx, Jy, Jz, e->device,
                                      (cudaStream_t)stream);
     if (err != cudaSuccess) return cuda_fail(err, "current deposition");
+    return ok();
+}
+
+boris_status boris_push_deposit(boris_ensemble *e, const boris_field *grid, double dt, void *Jx,
+                                void *Jy, void *Jz, double *d_diag, void *stream) {
+    if (!e || !grid || !Jx || !Jy || !Jz) return fail(BORIS_E_INVALID_ARG, "NULL argument");
+    if (grid->kind != FK_GRID) return fail(BORIS_E_INVALID_ARG, "field is not a grid");
+    boris_status s = check_push_args(e, grid, dt, 1);
+    if (s != BORIS_OK) return s;
+    if (e->memory != BORIS_MEMORY_DEVICE)
+        return fail(BORIS_E_UNSUPPORTED, "push + deposition needs a device-resident ensemble");
+    DeviceGuard g(e->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    DiagOut diag = {e->partials, e->partials_cap, 0};
+    DiagOut *dp = d_diag ? &diag : nullptr;
+    cudaError_t err =
+        e->precision == BORIS_FP32
+            ? push_deposit_view<float>(e, grid, dt, Jx, Jy, Jz, dp, st)
+            : push_deposit_view<double>(e, grid, dt, Jx, Jy, Jz, dp, st);
+    if (err != cudaSuccess) return cuda_fail(err, "push + deposition launch");
+    if (d_diag) {
+        err = e->n == 0 ? cudaMemsetAsync(d_diag, 0, 2 * sizeof(double), st)
+                        : launch_diag_finalize(diag.partials, diag.written, d_diag, st);
+        if (err != cudaSuccess) return cuda_fail(err, "diag finalize");
+    }
+    e->time += dt;
     return ok();
 }
 

@@ -131,6 +131,15 @@ struct DepCoefs {
     FP half_dt;
     DepCoef<FP> t[kMaxTypes];
 };
+// Fused grid-gather push + current deposition (SoA, 16 B-aligned; else
+// cudaErrorNotSupported).  J zeroed by the caller.
+template <typename FP>
+cudaError_t launch_push_deposit_soa(const EnsView &e, const GridArgs<FP> &g, const Coefs<FP> &co,
+                                    const DepCoefs<FP> &dc, void *Jx, void *Jy, void *Jz,
+                                    bool multi, DiagOut *diag, int device, cudaStream_t st);
+template <typename FP>
+cudaError_t launch_zero3(void *Jx, void *Jy, void *Jz, int64_t n, cudaStream_t st);
+
 template <typename FP>
 cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
                            void *Jx, void *Jy, void *Jz, int device, cudaStream_t st);

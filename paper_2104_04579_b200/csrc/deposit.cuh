@@ -1,0 +1,123 @@
+// deposit.cuh -- run-accumulating CIC current deposition of one lane (SURVEY §8(f)
+// row 4; reading c-dep in DESIGN.md): q w v^{n+1/2} at the half-
+// step position r^{n+1/2} = r^{n+1} - (dt/2) v^{n+1/2}, divided by the cell volume,
+// onto the 8 nodes of the particle's cell.  A lane keeps the 8 x 3 node sums of its
+// current cell in registers and issues atomics only when the cell changes
+// (`add`), or at the end of a warp tile after merging with the neighbouring lanes
+// that hold the same cell (`warp_merge` + `flush`).  Shared by the standalone
+// deposition kernel (k_grid.cu) and the fused push + deposit kernel.
+#pragma once
+
+#include "boris_internal.h"
+
+namespace boris {
+
+constexpr uint32_t kNoNode = 0xFFFFFFFFu;
+
+template <typename FP>
+struct DepositRun {
+    FP acc[8][3];
+    int cx[2], cy[2], cz[2];  // the open cell's node indices (cx[0] < 0: none)
+
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+        cx[0] = cx[1] = -1;
+        cy[0] = cy[1] = cz[0] = cz[1] = 0;
+    }
+
+    // Atomics for the open cell (if any), then zero the sums.
+    __device__ __forceinline__ void flush(const GridArgs<FP> &g, FP *Jx, FP *Jy, FP *Jz) {
+        if (cx[0] < 0) return;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const uint32_t row =
+                    ((uint32_t)cz[c] * (uint32_t)g.n[1] + (uint32_t)cy[b]) * (uint32_t)g.n[0];
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const int q = (c * 2 + b) * 2 + a;
+                    const uint32_t node = row + (uint32_t)cx[a];
+                    atomicAdd(Jx + node, acc[q][0]);
+                    atomicAdd(Jy + node, acc[q][1]);
+                    atomicAdd(Jz + node, acc[q][2]);
+                    acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+                }
+            }
+    }
+
+    // One particle (state after the push: r^{n+1}, p^{n+1/2}, weight w).
+    __device__ __forceinline__ void add(const GridArgs<FP> &g, const DepCoef<FP> &t, FP half_dt,
+                                        FP x, FP y, FP z, FP px, FP py, FP pz, FP w, FP *Jx,
+                                        FP *Jy, FP *Jz) {
+        const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
+        // v = p/(gamma m) = u/(S m gamma)
+        const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
+        const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
+        int ix[2], iy[2], iz[2];
+        FP fx, fy, fz;
+        grid_axis<FP>(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0], g.n[0],
+                      ix[0], ix[1], fx);
+        grid_axis<FP>(b_fma(-half_dt, vy, y), g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1], g.n[1],
+                      iy[0], iy[1], fy);
+        grid_axis<FP>(b_fma(-half_dt, vz, z), g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2], g.n[2],
+                      iz[0], iz[1], fz);
+        if (ix[0] != cx[0] || iy[0] != cy[0] || iz[0] != cz[0]) {
+            flush(g, Jx, Jy, Jz);
+            cx[0] = ix[0]; cx[1] = ix[1];
+            cy[0] = iy[0]; cy[1] = iy[1];
+            cz[0] = iz[0]; cz[1] = iz[1];
+        }
+        const FP wx[2] = {b_add(FP(1), -fx), fx};
+        const FP wy[2] = {b_add(FP(1), -fy), fy};
+        const FP wz[2] = {b_add(FP(1), -fz), fz};
+        const FP qw = b_mul(t.q_vol, w);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const FP wyz = b_mul(qw, b_mul(wy[b], wz[c]));
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const int q = (c * 2 + b) * 2 + a;
+                    const FP sw = b_mul(wx[a], wyz);
+                    acc[q][0] = b_fma(sw, vx, acc[q][0]);
+                    acc[q][1] = b_fma(sw, vy, acc[q][1]);
+                    acc[q][2] = b_fma(sw, vz, acc[q][2]);
+                }
+            }
+    }
+
+    // End of a warp tile (all 32 lanes): lanes holding the same open cell in
+    // consecutive lanes (contiguous when sorted) are summed with a segmented
+    // scan; every lane but each segment's last drops its cell, so the following
+    // flush() issues one set of atomics per segment.
+    __device__ __forceinline__ void warp_merge(const GridArgs<FP> &g, int lane) {
+        const unsigned full = 0xffffffffu;
+        const uint32_t key = cx[0] < 0 ? kNoNode
+                                       : ((uint32_t)cz[0] * (uint32_t)g.n[1] + (uint32_t)cy[0]) *
+                                                 (uint32_t)g.n[0] + (uint32_t)cx[0];
+        const uint32_t prev = __shfl_up_sync(full, key, 1);
+        const uint32_t next = __shfl_down_sync(full, key, 1);
+        const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
+        const int seg = 31 - __clz(heads & (full >> (31 - lane)));
+        // only as many scan rounds as the longest segment needs (warp-uniform)
+        const int span = (int)__reduce_max_sync(full, (unsigned)(lane - seg));
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            if (off > span) break;
+            const bool take = lane - off >= seg;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const FP v = __shfl_up_sync(full, acc[q][d], off);
+                    if (take) acc[q][d] = b_add(acc[q][d], v);
+                }
+        }
+        if (!(lane == 31 || next != key)) cx[0] = -1;  // not a segment tail: no flush
+    }
+};
+
+}  // namespace boris

@@ -12,6 +12,7 @@
 #include <type_traits>
 
 #include "boris_internal.h"
+#include "deposit.cuh"
 
 namespace boris {
 
@@ -439,7 +440,6 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
 // common case for particles sorted by cell) are summed with a segmented shuffle
 // scan and only each segment's last lane issues the atomics.  Equal nodes in
 // non-contiguous lanes simply stay separate segments (still correct).
-constexpr uint32_t kNoNode = 0xFFFFFFFFu;
 
 template <typename FP>
 __device__ __forceinline__ void warp_scatter_add(uint32_t node, FP vx, FP vy, FP vz, FP *Jx,
@@ -662,29 +662,8 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
             }
             __syncwarp();
         }
-        FP acc[8][3];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
-        int cx[2] = {-1, -1}, cy[2] = {0, 0}, cz[2] = {0, 0};
-        auto flush = [&]() {
-            if (cx[0] < 0) return;
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    const uint32_t row =
-                        ((uint32_t)cz[c] * (uint32_t)g.n[1] + (uint32_t)cy[b]) * (uint32_t)g.n[0];
-#pragma unroll
-                    for (int a = 0; a < 2; ++a) {
-                        const int q = (c * 2 + b) * 2 + a;
-                        const uint32_t node = row + (uint32_t)cx[a];
-                        atomicAdd(Jx + node, acc[q][0]);
-                        atomicAdd(Jy + node, acc[q][1]);
-                        atomicAdd(Jz + node, acc[q][2]);
-                        acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
-                    }
-                }
-        };
+        DepositRun<FP> run;
+        run.reset();
         constexpr int kUnrollJ = DIRECT ? R::K : 1;  // register arrays need constant indices
 #pragma unroll kUnrollJ
         for (int j = 0; j < R::K; ++j) {
@@ -699,70 +678,11 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
             const FP pz = DIRECT ? rv[5][j] : s[warp][5][sp];
             const FP w = DIRECT ? rv[6][j] : s[warp][6][sp];
             const DepCoef<FP> t = dc.t[multi ? (DIRECT ? rty[j] : s_ty[warp][sp]) : 0];
-            const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
-            const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
-            const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
-            int ix[2], iy[2], iz[2];
-            FP fx, fy, fz;
-            grid_axis<FP>(b_fma(-dc.half_dt, vx, x), g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0],
-                          g.n[0], ix[0], ix[1], fx);
-            grid_axis<FP>(b_fma(-dc.half_dt, vy, y), g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1],
-                          g.n[1], iy[0], iy[1], fy);
-            grid_axis<FP>(b_fma(-dc.half_dt, vz, z), g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2],
-                          g.n[2], iz[0], iz[1], fz);
-            if (ix[0] != cx[0] || iy[0] != cy[0] || iz[0] != cz[0]) {
-                flush();
-                cx[0] = ix[0]; cx[1] = ix[1];
-                cy[0] = iy[0]; cy[1] = iy[1];
-                cz[0] = iz[0]; cz[1] = iz[1];
-            }
-            const FP wx[2] = {b_add(FP(1), -fx), fx};
-            const FP wy[2] = {b_add(FP(1), -fy), fy};
-            const FP wz[2] = {b_add(FP(1), -fz), fz};
-            const FP qw = b_mul(t.q_vol, w);
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    const FP wyz = b_mul(qw, b_mul(wy[b], wz[c]));
-#pragma unroll
-                    for (int a = 0; a < 2; ++a) {
-                        const int q = (c * 2 + b) * 2 + a;
-                        const FP sw = b_mul(wx[a], wyz);
-                        acc[q][0] = b_fma(sw, vx, acc[q][0]);
-                        acc[q][1] = b_fma(sw, vy, acc[q][1]);
-                        acc[q][2] = b_fma(sw, vz, acc[q][2]);
-                    }
-                }
+            run.add(g, t, dc.half_dt, x, y, z, px, py, pz, w, Jx, Jy, Jz);
         }
-        // End of tile: lanes still holding the same cell (contiguous when sorted) are
-        // summed with a warp segmented scan; only each segment's last lane flushes.
-        {
-            const unsigned full = 0xffffffffu;
-            const uint32_t key = cx[0] < 0 ? kNoNode
-                                           : ((uint32_t)cz[0] * (uint32_t)g.n[1] + (uint32_t)cy[0]) *
-                                                     (uint32_t)g.n[0] + (uint32_t)cx[0];
-            const uint32_t prev = __shfl_up_sync(full, key, 1);
-            const uint32_t next = __shfl_down_sync(full, key, 1);
-            const unsigned heads = __ballot_sync(full, lane == 0 || prev != key);
-            const int seg = 31 - __clz(heads & (full >> (31 - lane)));
-            // only as many scan rounds as the longest segment needs (warp-uniform)
-            const int span = (int)__reduce_max_sync(full, (unsigned)(lane - seg));
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                if (off > span) break;
-                const bool take = lane - off >= seg;
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        const FP v = __shfl_up_sync(full, acc[q][d], off);
-                        if (take) acc[q][d] = b_add(acc[q][d], v);
-                    }
-            }
-            if (!(lane == 31 || next != key)) cx[0] = -1;  // not a segment tail: no flush
-        }
-        flush();
+        // end of tile: merge lanes holding the same cell, one flush per segment
+        run.warp_merge(g, lane);
+        run.flush(g, Jx, Jy, Jz);
         __syncwarp();
     }
 }
@@ -777,14 +697,22 @@ __global__ void k_zero3(FP *a, FP *b, FP *c, int64_t n) {
     }
 }
 
+// Zero J: one launch for the three arrays (three memsets cost ~3 launch gaps).
+template <typename FP>
+cudaError_t launch_zero3(void *Jx, void *Jy, void *Jz, int64_t n, cudaStream_t st) {
+    const int64_t blocks = (n + 255) / 256;
+    k_zero3<FP><<<(unsigned)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, st>>>(
+        (FP *)Jx, (FP *)Jy, (FP *)Jz, n);
+    return cudaGetLastError();
+}
+template cudaError_t launch_zero3<float>(void *, void *, void *, int64_t, cudaStream_t);
+template cudaError_t launch_zero3<double>(void *, void *, void *, int64_t, cudaStream_t);
+
 template <typename FP>
 cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
                            void *Jx, void *Jy, void *Jz, int device, cudaStream_t st) {
     const int64_t ncell = (int64_t)g.n[0] * g.n[1] * g.n[2];
-    // zero J: one launch for the three arrays (three memsets cost ~3 launch gaps)
-    k_zero3<FP><<<(unsigned)((ncell + 255) / 256 < 4096 ? (ncell + 255) / 256 : 4096), 256, 0,
-                  st>>>((FP *)Jx, (FP *)Jy, (FP *)Jz, ncell);
-    cudaError_t err = cudaGetLastError();
+    cudaError_t err = launch_zero3<FP>(Jx, Jy, Jz, ncell, st);
     if (err != cudaSuccess || e.n == 0) return err;
     if (e.layout == BORIS_LAYOUT_SOA && deposit_runs_enabled()) {
         using R = DepRuns<FP>;

@@ -9,6 +9,7 @@
 // group are issued before any arithmetic (12 x LDG.128 in flight per thread).
 // Grid-stride over groups with a grid sized to the resident-block count.
 #include "boris_internal.h"
+#include "deposit.cuh"
 
 namespace boris {
 
@@ -248,6 +249,159 @@ template cudaError_t launch_stream_soa_grid<float>(const EnsView &, const GridAr
 template cudaError_t launch_stream_soa_grid<double>(const EnsView &, const GridArgs<double> &,
                                                     const Coefs<double> &, bool, DiagOut *, int,
                                                     cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// Fused PIC particle step: grid-gather push (as k_stream_soa_grid) followed, in the
+// same thread and registers, by the CIC current deposition of the new state (as
+// k_deposit_runs): r, p, w are not re-read and the deposition costs no launch.
+// The state is bitwise the push's; J differs from push + deposit only in the
+// order of its float atomics.  Warp-uniform grid-stride loop (every lane takes
+// part in the end-of-group segmented merge).
+// ---------------------------------------------------------------------------
+template <typename FP, bool MULTI, bool DIAG>
+__global__ void __launch_bounds__(kStreamThreads, 2)
+    k_push_deposit_soa(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
+                       const __grid_constant__ Coefs<FP> co, const __grid_constant__ DepCoefs<FP> dc,
+                       FP *Jx, FP *Jy, FP *Jz, int64_t n_groups, int64_t n, double *partials) {
+    constexpr int V = Vec<FP>::N;
+    __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
+    __shared__ DepCoef<FP> s_d[MULTI ? kMaxTypes : 1];
+    if (MULTI) {
+        for (int k = threadIdx.x; k < dc.n_types; k += blockDim.x) s_d[k] = dc.t[k];
+        load_type_table(co, s_t);  // ends with __syncthreads
+    }
+    const int lane = threadIdx.x & 31;
+    FP *X = (FP *)s.x, *Y = (FP *)s.y, *Z = (FP *)s.z;
+    FP *PX = (FP *)s.px, *PY = (FP *)s.py, *PZ = (FP *)s.pz, *G = (FP *)s.g;
+    const FP *W = (const FP *)s.w;
+    double ke = 0.0, cnt = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
+    for (int64_t g0 = (int64_t)blockIdx.x * kStreamThreads + (threadIdx.x & ~31); g0 < n_groups;
+         g0 += stride) {
+        const int64_t grp = g0 + lane;
+        const bool valid = grp < n_groups;
+        DepositRun<FP> run;
+        run.reset();
+        if (valid) {
+            const int64_t i0 = grp * V;
+            Vec<FP> x, y, z, px, py, pz, w, gm;
+            x.load_state(X + i0);
+            y.load_state(Y + i0);
+            z.load_state(Z + i0);
+            px.load_state(PX + i0);
+            py.load_state(PY + i0);
+            pz.load_state(PZ + i0);
+            int ty[V];
+            if (MULTI) load_types<V>(s.type + i0, ty);
+            if (W) w.load_field(W + i0);
+            else {
+#pragma unroll
+                for (int j = 0; j < V; ++j) w.v[j] = FP(1);
+            }
+            FP ex[V], ey[V], ez[V], bx[V], by[V], bz[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                grid_gather<FP>(g, x.v[j], y.v[j], z.v[j], ex[j], ey[j], ez[j], bx[j], by[j],
+                                bz[j]);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const TypeCoef<FP> tc = MULTI ? s_t[ty[j]] : co.t[0];
+                FP ux, uy, uz;
+                push_one<FP>(x.v[j], y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], gm.v[j], ex[j],
+                             ey[j], ez[j], bx[j], by[j], bz[j], tc, ux, uy, uz);
+                if (DIAG) {
+                    ke += (double)kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j], tc);
+                    cnt += 1.0;
+                }
+            }
+            x.store(X + i0);
+            y.store(Y + i0);
+            z.store(Z + i0);
+            px.store(PX + i0);
+            py.store(PY + i0);
+            pz.store(PZ + i0);
+            gm.store(G + i0);
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                run.add(g, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j], y.v[j], z.v[j],
+                        px.v[j], py.v[j], pz.v[j], w.v[j], Jx, Jy, Jz);
+        }
+        run.warp_merge(g, lane);
+        run.flush(g, Jx, Jy, Jz);
+    }
+    // ragged tail (n mod V particles): push then deposit directly
+    const int64_t tail0 = n_groups * V;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail0) {
+        const int64_t i = tail0 + threadIdx.x;
+        const int ty = MULTI ? s.type[i] : 0;
+        const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
+        FP ux, uy, uz, gam, Ex, Ey, Ez, Bx, By, Bz;
+        FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
+        const FP w = W ? W[i] : FP(1);
+        grid_gather<FP>(g, x, y, z, Ex, Ey, Ez, Bx, By, Bz);
+        push_one<FP>(x, y, z, px, py, pz, gam, Ex, Ey, Ez, Bx, By, Bz, tc, ux, uy, uz);
+        X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
+        if (DIAG) {
+            ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, w, tc);
+            cnt += 1.0;
+        }
+        DepositRun<FP> run;
+        run.reset();
+        run.add(g, MULTI ? s_d[ty] : dc.t[0], dc.half_dt, x, y, z, px, py, pz, w, Jx, Jy, Jz);
+        run.flush(g, Jx, Jy, Jz);
+    }
+    if (DIAG) block_diag_partial<kStreamThreads>(ke, cnt, partials);
+}
+
+template <typename FP, bool MULTI, bool DIAG>
+static cudaError_t dispatch_push_deposit(const EnsView &e, const GridArgs<FP> &g,
+                                         const Coefs<FP> &co, const DepCoefs<FP> &dc, FP *J[3],
+                                         DiagOut *diag, int device, cudaStream_t st) {
+    constexpr int V = Vec<FP>::N;
+    const int64_t n_groups = e.n / V;
+    const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
+    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2, device);
+    if (DIAG && grid > diag->cap) grid = diag->cap;
+    k_push_deposit_soa<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
+        e.soa, g, co, dc, J[0], J[1], J[2], n_groups, e.n, diag ? diag->partials : nullptr);
+    if (diag) diag->written = DIAG ? grid : 0;
+    return cudaGetLastError();
+}
+
+// Returns cudaErrorNotSupported when the state arrays are not 16 B aligned (the
+// caller then runs the push and the deposition as two launches).  J is zeroed
+// by the caller.
+template <typename FP>
+cudaError_t launch_push_deposit_soa(const EnsView &e, const GridArgs<FP> &g, const Coefs<FP> &co,
+                                    const DepCoefs<FP> &dc, void *Jx, void *Jy, void *Jz,
+                                    bool multi, DiagOut *diag, int device, cudaStream_t st) {
+    constexpr int V = Vec<FP>::N;
+    if (e.n == 0) {
+        if (diag) diag->written = 0;
+        return cudaSuccess;
+    }
+    const bool al = aligned16(e.soa.x) && aligned16(e.soa.y) && aligned16(e.soa.z) &&
+                    aligned16(e.soa.px) && aligned16(e.soa.py) && aligned16(e.soa.pz) &&
+                    aligned16(e.soa.g) && (!e.soa.w || aligned16(e.soa.w)) &&
+                    (!multi || ((uintptr_t)e.soa.type & (2 * V - 1)) == 0);
+    if (!al) return cudaErrorNotSupported;
+    FP *J[3] = {(FP *)Jx, (FP *)Jy, (FP *)Jz};
+    const bool d = diag != nullptr;
+    if (multi)
+        return d ? dispatch_push_deposit<FP, true, true>(e, g, co, dc, J, diag, device, st)
+                 : dispatch_push_deposit<FP, true, false>(e, g, co, dc, J, diag, device, st);
+    return d ? dispatch_push_deposit<FP, false, true>(e, g, co, dc, J, diag, device, st)
+             : dispatch_push_deposit<FP, false, false>(e, g, co, dc, J, diag, device, st);
+}
+
+template cudaError_t launch_push_deposit_soa<float>(const EnsView &, const GridArgs<float> &,
+                                                    const Coefs<float> &, const DepCoefs<float> &,
+                                                    void *, void *, void *, bool, DiagOut *, int,
+                                                    cudaStream_t);
+template cudaError_t launch_push_deposit_soa<double>(const EnsView &, const GridArgs<double> &,
+                                                     const Coefs<double> &,
+                                                     const DepCoefs<double> &, void *, void *,
+                                                     void *, bool, DiagOut *, int, cudaStream_t);
 
 // Unaligned inputs (e.g. sliced torch tensors): one particle per thread, scalar
 // accesses, the same push_one arithmetic.

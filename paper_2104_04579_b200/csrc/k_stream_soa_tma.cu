@@ -203,7 +203,11 @@ cudaError_t launch_stream_soa_tma(const EnsView &e, const FieldSoaPtrs &f, const
 template <typename FP>
 struct GridTma {
     static constexpr int THREADS = 256;
+#ifdef BORIS_GRID_TMA_TP
+    static constexpr int TP = BORIS_GRID_TMA_TP / (sizeof(FP) / 4);
+#else
     static constexpr int TP = sizeof(FP) == 4 ? 512 : 256;  // particles per tile
+#endif
     static constexpr int PPT = TP / THREADS;
     static constexpr int ARR = TP * (int)sizeof(FP);
     static constexpr int NSLOT = 8;  // 0-5 state, 6 weight, 7 gamma (out)

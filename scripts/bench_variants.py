@@ -102,7 +102,7 @@ def streaming(name, layout, precision, n, diag=False, types=None, iters=20):
             "frac_of_measured_peak": gbs / peak(), "frac_of_8TBs": gbs / 8000.0}
 
 
-def fused(name, cfg, layout, precision, n, steps, iters=5, field_kind=None):
+def fused(name, cfg, layout, precision, n, steps, iters=5, field_kind=None, flags=0):
     w = synth.config(cfg, n=n)
     if field_kind == "mdipole":
         k = synth.OMEGA0 / synth.C_LIGHT
@@ -110,12 +110,15 @@ def fused(name, cfg, layout, precision, n, steps, iters=5, field_kind=None):
         w.plane_wave = dict(A0=k * math.sqrt(3e21 / synth.C_LIGHT), omega0=synth.OMEGA0, k=k)
     ens, field = make(w, layout, precision, n)
     sp = torch.cuda.current_stream().cuda_stream
-    ms = time_launches(lambda: lb.boris_push(ens.handle, field, w.dt, steps, sp), iters, warmup=1)
+    ms = time_launches(lambda: lb.boris_push_ex(ens.handle, field, w.dt, steps, flags, None, sp),
+                       iters, warmup=1)
     ens.close()
     lb.boris_field_destroy(field)
     ups = n * steps / (ms * 1e-3)
     return {"variant": name, "layout": layout, "precision": precision, "n": n,
             "field": w.field_kind, "steps_per_launch": steps, "n_types": len(w.types),
+            "pusher": {0: "boris", lb.BORIS_PUSH_PUSHER_VAY: "vay",
+                       lb.BORIS_PUSH_PUSHER_HIGUERA_CARY: "higuera-cary"}[flags],
             "ms_per_launch": ms, "ps_per_particle_step": 1e12 / ups,
             "particle_updates_per_s": ups}
 
@@ -148,6 +151,13 @@ def main():
                       field_kind="mdipole"))
     rows.append(fused("mdipole-soa-fp64-100", "C4", "soa", "fp64", n1 // 10, 100,
                       field_kind="mdipole"))
+    # alternative pushers (generic-orientation fused kernels)
+    for pname, fl in (("vay", lb.BORIS_PUSH_PUSHER_VAY),
+                      ("hc", lb.BORIS_PUSH_PUSHER_HIGUERA_CARY)):
+        rows.append(fused(f"C4-soa-fp32-planewave-100-{pname}", "C4", "soa", "fp32", n1, 100,
+                          flags=fl))
+        rows.append(fused(f"C3-aos-fp64-crossed-100-{pname}", "C3", "aos", "fp64", 10_000_000,
+                          100, flags=fl))
     for r in rows:
         print(json.dumps(r), flush=True)
 

@@ -30,6 +30,10 @@ if [ $what = ncu ] || [ $what = all ]; then
     timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c 1 \
       -o gpurun_out/prof2/$name -f "$@" > gpurun_out/prof2/$name.log 2>&1
     echo "ncu $name rc=$?"
+    # keep the CSV pages, not the report (gpurun copies back at most 64 MiB)
+    $NCU -i gpurun_out/prof2/$name.ncu-rep --page raw --csv > gpurun_out/prof2/${name}_raw.csv 2>/dev/null
+    $NCU -i gpurun_out/prof2/$name.ncu-rep --page details --csv > gpurun_out/prof2/${name}_details.csv 2>/dev/null
+    rm -f gpurun_out/prof2/$name.ncu-rep
   }
   PK="python scripts/prof_kernels.py --case"
   PF="python scripts/prof_fused.py"

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--sort-every", type=int, default=10)
     ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--fused", action="store_true",
+                    help="push + deposit in one call (boris_push_deposit)")
     a = ap.parse_args()
     prec = lb.BORIS_FP32 if a.precision == "fp32" else lb.BORIS_FP64
     dt_ = torch.float32 if prec == lb.BORIS_FP32 else torch.float64
@@ -59,16 +61,23 @@ def main():
     for step in range(a.steps + 2):  # 2 warm-up steps
         if step % a.sort_every == 0:
             timed("sort", lambda: lb.boris_ensemble_sort_by_cell(ens.handle, grid, sp))
-        timed("push", lambda: lb.boris_push_diag(ens.handle, grid, w.dt, 1, diag.data_ptr(), sp))
-        timed("deposit", lambda: lb.boris_deposit_current(ens.handle, grid, w.dt,
-                                                          *(j.data_ptr() for j in J), sp))
+        if a.fused:
+            timed("push", lambda: lb.boris_push_deposit(ens.handle, grid, w.dt,
+                                                        *(j.data_ptr() for j in J),
+                                                        diag.data_ptr(), sp))
+        else:
+            timed("push", lambda: lb.boris_push_diag(ens.handle, grid, w.dt, 1, diag.data_ptr(),
+                                                     sp))
+            timed("deposit", lambda: lb.boris_deposit_current(ens.handle, grid, w.dt,
+                                                              *(j.data_ptr() for j in J), sp))
         if step == 1:
             torch.cuda.synchronize()
             ev = {k: [] for k in ev}
     torch.cuda.synchronize()
     ms = {k: sum(a0.elapsed_time(a1) for a0, a1 in v) for k, v in ev.items()}
     total = sum(ms.values())
-    out = {"exp": "pic_particle_cycle", "precision": a.precision, "n": a.n, "cells": g ** 3,
+    out = {"exp": "pic_particle_cycle", "precision": a.precision, "fused": a.fused,
+           "n": a.n, "cells": g ** 3,
            "steps": a.steps, "sort_every": a.sort_every,
            "ms_per_step": {k: v / a.steps for k, v in ms.items()},
            "ps_per_particle_step": total * 1e9 / (a.n * a.steps),

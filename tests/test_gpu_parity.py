@@ -925,6 +925,103 @@ def test_deposit_current_runs_and_contention(precision, mode, layout):
 
 
 # ---------------------------------------------------------------------------
+# Fused PIC particle step: grid push + current deposition in one kernel.
+# ---------------------------------------------------------------------------
+
+def _deposit_bound(d, w, params, precision):
+    """Summation-error bound per J component: tol x sum over particles of
+    |q w v| / cell volume (as test_deposit_current_runs_and_contention)."""
+    pos, mom = stack3(d, "x", "y", "z"), stack3(d, "px", "py", "pz")
+    typ = d["type"].numpy().astype(np.int64)
+    tq = np.array([t[0] for t in w.types])
+    tm = np.array([t[1] for t in w.types])
+    m = tm[typ][:, None]
+    gam = np.sqrt(1.0 + ((mom / (m * w.light_velocity)) ** 2).sum(1))[:, None]
+    vol = params[3] * params[4] * params[5]
+    single = (np.abs(tq[typ])[:, None] * d["weight"].numpy()[:, None] * np.abs(mom / (m * gam))) / vol
+    tol = 1e-5 if precision == "fp32" else 1e-12
+    return tol * single.sum(0), pos, mom, typ, tq, tm
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("order", ["sorted", "unsorted"])
+@pytest.mark.parametrize("n", [N_SMALL, 5])
+def test_push_deposit_equals_push_then_deposit(precision, layout, order, n):
+    """boris_push_deposit == boris_push (1 step, grid field) then boris_deposit_current:
+    state bitwise, J to the float summation-order bound, and J against the oracle's
+    deposition of the pushed state; the diagnostic matches boris_push_diag.  Three
+    types, ragged n (fused SoA kernel; AoS takes the two-launch path)."""
+    h, params, _, _ = grid_setup(precision)
+    w = synth.config("C5")
+    w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
+    w.type_mix = "random"
+    d = rounded(w.generate(0, n), precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    a = cls(n, PREC[precision], w.types, w.light_velocity, with_fields=False)
+    b = cls(n, PREC[precision], w.types, w.light_velocity, with_fields=False)
+    a.fill(d)
+    b.fill(d)
+    a.wrap()
+    b.wrap()
+    if order == "sorted":
+        lb.boris_ensemble_sort_by_cell(a.handle, h)
+        lb.boris_ensemble_sort_by_cell(b.handle, h)
+    nx, ny, nz = int(params[6]), int(params[7]), int(params[8])
+    dt_ = torch.float32 if precision == "fp32" else torch.float64
+    Ja = [torch.full((nz, ny, nx), 3.0, dtype=dt_, device="cuda") for _ in range(3)]
+    Jb = [torch.zeros((nz, ny, nx), dtype=dt_, device="cuda") for _ in range(3)]
+    da = torch.zeros(2, dtype=torch.float64, device="cuda")
+    db = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_deposit(a.handle, h, w.dt, *(j.data_ptr() for j in Ja), da.data_ptr())
+    lb.boris_push_diag(b.handle, h, w.dt, 1, db.data_ptr())
+    lb.boris_deposit_current(b.handle, h, w.dt, *(j.data_ptr() for j in Jb))
+    torch.cuda.synchronize()
+    sa, sb = a.state(), b.state()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma", "weight", "type"):
+        assert torch.equal(sa[k], sb[k]), k
+    assert lb.boris_ensemble_get_time(a.handle) == lb.boris_ensemble_get_time(b.handle) == w.dt
+    assert da[1].item() == n
+    assert da[0].item() == pytest.approx(db[0].item(), rel=1e-12)
+    after = {k: sa[k] for k in ("x", "y", "z", "px", "py", "pz", "weight", "type")}
+    bound, pos, mom, typ, tq, tm = _deposit_bound(after, w, params, precision)
+    Jga = torch.stack(Ja).double().cpu().numpy()
+    Jgb = torch.stack(Jb).double().cpu().numpy()
+    assert (np.abs(Jga - Jgb).reshape(3, -1).max(1) <= 2 * bound).all()
+    Jr = oracle.deposit_current(pos, mom, after["weight"].numpy(), typ, list(tq), list(tm),
+                                w.light_velocity, w.dt, params)
+    assert (np.abs(Jga - Jr).reshape(3, -1).max(1) <= bound).all()
+    a.close()
+    b.close()
+    lb.boris_field_destroy(h)
+
+
+def test_push_deposit_errors():
+    h, params, _, _ = grid_setup("fp32")
+    w = synth.config("C2")
+    ens = SoaEnsemble(64, lb.BORIS_FP32, w.types, w.light_velocity)
+    ens.fill(rounded(w.generate(0, 64), "fp32"))
+    ens.wrap()
+    J = [torch.zeros(int(params[6] * params[7] * params[8]), device="cuda") for _ in range(3)]
+    with pytest.raises(lb.BorisError) as ei:    # not a grid
+        lb.boris_push_deposit(ens.handle, ens.field, w.dt, *(j.data_ptr() for j in J))
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
+    with pytest.raises(lb.BorisError) as ei:    # NULL J
+        lb.boris_push_deposit(ens.handle, h, w.dt, J[0].data_ptr(), None, J[2].data_ptr())
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
+    with pytest.raises(lb.BorisError) as ei:    # dt not finite
+        lb.boris_push_deposit(ens.handle, h, float("nan"), *(j.data_ptr() for j in J))
+    assert ei.value.status == lb.BORIS_E_INVALID_ARG
+    h64, *_ = grid_setup("fp64")
+    with pytest.raises(lb.BorisError) as ei:    # precision mismatch
+        lb.boris_push_deposit(ens.handle, h64, w.dt, *(j.data_ptr() for j in J))
+    assert ei.value.status == lb.BORIS_E_MISMATCH
+    ens.close()
+    lb.boris_field_destroy(h)
+    lb.boris_field_destroy(h64)
+
+
+# ---------------------------------------------------------------------------
 # Alternative pushers (SURVEY §8(f) row 4; readings c-vay, c-hc).
 # ---------------------------------------------------------------------------
 
