@@ -285,7 +285,7 @@ boris_status boris_deposit_current(const boris_ensemble *ens, const boris_field 
                                    void *Jx, void *Jy, void *Jz, void *stream);
 
 /*
- * Fused PIC particle step (PAPER.md L86-92: field interpolation to the particles,
+ * Fused PIC particle step (PAPER.md L89-92: field interpolation to the particles,
  * the push, and the current "computed and added to Maxwell's equations"): one
  * push of size dt with the field gathered from `grid` (as boris_push(ens, grid,
  * dt, 1, stream)) followed by the current deposition of the new state onto the

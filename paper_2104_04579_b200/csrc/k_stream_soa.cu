@@ -258,8 +258,11 @@ template cudaError_t launch_stream_soa_grid<double>(const EnsView &, const GridA
 // order of its float atomics.  Warp-uniform grid-stride loop (every lane takes
 // part in the end-of-group segmented merge).
 // ---------------------------------------------------------------------------
+#ifndef BORIS_PD_MINB
+#define BORIS_PD_MINB 2
+#endif
 template <typename FP, bool MULTI, bool DIAG>
-__global__ void __launch_bounds__(kStreamThreads, 2)
+__global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
     k_push_deposit_soa(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
                        const __grid_constant__ Coefs<FP> co, const __grid_constant__ DepCoefs<FP> dc,
                        FP *Jx, FP *Jy, FP *Jz, int64_t n_groups, int64_t n, double *partials) {
@@ -360,7 +363,7 @@ static cudaError_t dispatch_push_deposit(const EnsView &e, const GridArgs<FP> &g
     constexpr int V = Vec<FP>::N;
     const int64_t n_groups = e.n / V;
     const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
-    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2, device);
+    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, BORIS_PD_MINB, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
     k_push_deposit_soa<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
         e.soa, g, co, dc, J[0], J[1], J[2], n_groups, e.n, diag ? diag->partials : nullptr);

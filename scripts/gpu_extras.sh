@@ -21,6 +21,7 @@ fi
 if [ $what = pic ] || [ $what = all ]; then
   for se in 1 10 1000000; do
     timeout 600 python scripts/pic_cycle.py --sort-every $se >> gpurun_out/extras/pic_cycle.jsonl 2>> gpurun_out/extras/pic_cycle.err
+    timeout 600 python scripts/pic_cycle.py --sort-every $se --fused >> gpurun_out/extras/pic_cycle.jsonl 2>> gpurun_out/extras/pic_cycle.err
   done
   echo pic rc=$?
 fi
@@ -50,6 +51,8 @@ if [ $what = ncu ] || [ $what = all ]; then
   cap fused_mdipole_fp32 '^k_fused$' 1 $PF --field mdipole
   cap fused_mdipole_fp64 '^k_fused$' 1 $PF --field mdipole --precision fp64
   cap fused_uniform_C3_fp64 '^k_fused$' 1 $PF --field uniform --precision fp64
+  cap grid_fused20 '^k_fused$' 1 $PK grid --steps 20
+  cap push_deposit 'k_push_deposit' 3 python scripts/pic_cycle.py --fused --steps 3
 fi
 if [ $what = sanitize ] || [ $what = all ]; then
   for tool in memcheck racecheck synccheck initcheck; do

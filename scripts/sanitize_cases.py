@@ -102,6 +102,8 @@ def main():
                 lb.boris_push_diag(e.handle, grid, w.dt, 3, dp)
                 lb.boris_push_diag(e.handle, grid, w.dt, 1, dp)   # streaming grid step
                 lb.boris_deposit_current(e.handle, grid, w.dt, *(j.data_ptr() for j in J))
+                lb.boris_push_deposit(e.handle, grid, w.dt, *(j.data_ptr() for j in J), dp)
+                lb.boris_push_deposit(e.handle, grid, w.dt, *(j.data_ptr() for j in J))
                 lb.boris_field_evaluate(grid, e.handle, 0.0, e.field)
                 for flags in (lb.BORIS_PUSH_PUSHER_VAY, lb.BORIS_PUSH_PUSHER_HIGUERA_CARY):
                     lb.boris_push_ex(e.handle, e.field, w.dt, 2, flags, dp)
