@@ -18,12 +18,32 @@ template <typename FP>
 struct DepositRun {
     FP acc[8][3];
     int cx[2], cy[2], cz[2];  // the open cell's node indices (cx[0] < 0: none)
+    FP fl[3];                 // the open cell's unwrapped floor((r - org)/h)
 
     __device__ __forceinline__ void reset() {
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
         cx[0] = cx[1] = -1;
         cy[0] = cy[1] = cz[0] = cz[1] = 0;
+        fl[0] = fl[1] = fl[2] = FP(0);
+    }
+
+    // grid_axis split in two: the unwrapped floor and the weight f (every
+    // particle), the periodic wrap to node indices (only when the cell changes).
+    static __device__ __forceinline__ FP axis_floor(FP x, FP org, FP inv_h, FP &f) {
+        const FP xi = b_mul(b_add(x, -org), inv_h);
+        const FP l = floor(xi);
+        f = b_add(xi, -l);  // exact, in [0, 1)
+        return l;
+    }
+    static __device__ __forceinline__ void axis_wrap(FP l, FP nf, FP inv_nf, int n, int &i0,
+                                                     int &i1) {
+        const FP w = b_fma(-nf, floor(b_mul(l, inv_nf)), l);  // l mod n, up to +-1 rounding
+        int i = (int)w;
+        if (i >= n) i -= n;
+        if (i < 0) i += n;
+        i0 = i;
+        i1 = (i + 1 == n) ? 0 : i + 1;
     }
 
     // Atomics for the open cell (if any), then zero the sums.
@@ -55,19 +75,18 @@ struct DepositRun {
         // v = p/(gamma m) = u/(S m gamma)
         const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
         const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
-        int ix[2], iy[2], iz[2];
         FP fx, fy, fz;
-        grid_axis<FP>(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0], g.n[0],
-                      ix[0], ix[1], fx);
-        grid_axis<FP>(b_fma(-half_dt, vy, y), g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1], g.n[1],
-                      iy[0], iy[1], fy);
-        grid_axis<FP>(b_fma(-half_dt, vz, z), g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2], g.n[2],
-                      iz[0], iz[1], fz);
-        if (ix[0] != cx[0] || iy[0] != cy[0] || iz[0] != cz[0]) {
+        const FP lx = axis_floor(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], fx);
+        const FP ly = axis_floor(b_fma(-half_dt, vy, y), g.org[1], g.inv_h[1], fy);
+        const FP lz = axis_floor(b_fma(-half_dt, vz, z), g.org[2], g.inv_h[2], fz);
+        // same unwrapped cell -> same nodes; a periodic image of the open cell only
+        // costs an extra flush
+        if (cx[0] < 0 || lx != fl[0] || ly != fl[1] || lz != fl[2]) {
             flush(g, Jx, Jy, Jz);
-            cx[0] = ix[0]; cx[1] = ix[1];
-            cy[0] = iy[0]; cy[1] = iy[1];
-            cz[0] = iz[0]; cz[1] = iz[1];
+            fl[0] = lx; fl[1] = ly; fl[2] = lz;
+            axis_wrap(lx, g.nf[0], g.inv_nf[0], g.n[0], cx[0], cx[1]);
+            axis_wrap(ly, g.nf[1], g.inv_nf[1], g.n[1], cy[0], cy[1]);
+            axis_wrap(lz, g.nf[2], g.inv_nf[2], g.n[2], cz[0], cz[1]);
         }
         const FP wx[2] = {b_add(FP(1), -fx), fx};
         const FP wy[2] = {b_add(FP(1), -fy), fy};

@@ -2,6 +2,7 @@
 """Summarise ncu --set full reports (one launch each) into a markdown table.
 
     python scripts/ncu_summary.py gpurun_out/prof2/*.ncu-rep > profiles/r01/kernels_ncu.md
+    python scripts/ncu_summary.py gpurun_out/prof2/*_raw.csv    # `--page raw --csv` exports
 """
 import csv
 import io
@@ -35,14 +36,17 @@ def to_gb(val, unit):
 def main():
     rows = []
     for path in sys.argv[1:]:
-        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                             text=True).stdout
+        if path.endswith(".csv"):
+            out = open(path).read()
+        else:
+            out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                                 capture_output=True, text=True).stdout
         r = list(csv.reader(io.StringIO(out)))
         if len(r) < 3:
             continue
         hdr, units, vals = r[0], r[1], r[2]
         d = {h: (u, v) for h, u, v in zip(hdr, units, vals)}
-        name = os.path.basename(path).replace(".ncu-rep", "")
+        name = os.path.basename(path).replace(".ncu-rep", "").replace("_raw.csv", "")
         kern = d.get("Kernel Name", ("", "?"))[1][:60]
         row = {"case": name, "kernel": kern}
         for label, key, mult, _ in METRICS:
