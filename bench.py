@@ -128,6 +128,16 @@ def cpu_baseline(workload, target_s=15.0, sample=1 << 21, threads=None):
                       f"oracle, per-particle fields, OpenMP {threads} threads, {el:.1f} s)"}
 
 
+def arm_config(w, n_local, world, bpp):
+    """The `config` object of the JSON line (the same for both arms)."""
+    return {"workload": f"{w.name}: BASELINE configs[4]" if w.name == "C5" else w.name,
+            "particles_total": w.n, "particles_per_gpu": n_local,
+            "layout": "SoA", "field": "per-particle E/B arrays",
+            "steps_per_launch": 1, "diagnostic": "per-step KE + count allreduce",
+            "parallelism": f"shard{world}", "l2": "inputs larger than L2 "
+            f"({bpp * n_local / 1e9:.1f} GB per GPU per step vs 126 MB)"}
+
+
 def run_reference(args):
     """--impl reference: the oracle timed as the reference arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", 0))
@@ -138,6 +148,7 @@ def run_reference(args):
     import synth
     import oracle
     w = synth.config(args.workload, n=args.particles)
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
     threads = os.cpu_count() or 1
     sample = args.ref_sample
     d = w.generate(0, sample)
@@ -165,11 +176,13 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "ns_per_particle_step": 1e9 / value,
-        "config": {"workload": f"{w.name} sample", "particles": sample,
-                   "field": "per-particle E/B", "layout": "canonical double",
-                   "note": "oracle (scalar double C, OpenMP) on a bounded sample of the workload"},
+        "config": arm_config(w, w.n // world - (w.n // world) % 8, world,
+                             BYTES_PER_PARTICLE_STEP[w.name]),
         "cpu_baseline": {"value": value, "unit": unit, "cores": threads, "kind": "oracle",
-                         "sample": f"{sample} particles x {args.steps} steps of {w.name}"},
+                         "sample": f"{sample} particles x {args.steps} steps of {w.name} (fp64 "
+                                   "scalar C oracle, canonical double layout, per-particle "
+                                   "fields, OpenMP over the host cores; throughput scales "
+                                   "linearly in the particle count)"},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -333,12 +346,7 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "ns_per_particle_step": 1e9 / value,
             "hbm_gbs_per_gpu": achieved,
-            "config": {"workload": f"{w.name}: BASELINE configs[4]" if w.name == "C5" else w.name,
-                       "particles_total": w.n, "particles_per_gpu": n_local,
-                       "layout": "SoA", "field": "per-particle E/B arrays",
-                       "steps_per_launch": 1, "diagnostic": "per-step KE + count allreduce",
-                       "parallelism": f"shard{world}", "l2": "inputs larger than L2 "
-                       f"({bpp * n_local / 1e9:.1f} GB per GPU per step vs 126 MB)"},
+            "config": arm_config(w, n_local, world, bpp),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "frac_of_nominal_8tbs": achieved / 8000.0,
