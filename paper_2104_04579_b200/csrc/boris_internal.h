@@ -80,6 +80,21 @@ void scratch_free(void *ptr, cudaStream_t st);
 
 // Grid of a grid-stride launch: min(work blocks, SMs x resident blocks x waves).
 int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device);
+// Grid of an ALU-bound grid-stride launch: min(work blocks, SMs x the kernel's
+// resident blocks per SM) -- one wave, equal work per block.
+int64_t resident_grid(const void *kernel, int threads, int64_t work_blocks, int device);
+
+// Grid of the register-fused kernels (k_fused, k_fused_arrays; kFusedThreads
+// threads).  BORIS_FUSED_GRID (tuning): 0 one resident wave, 1 the 4-wave
+// grid-stride cap of stream_grid, 2 one block per work block (no grid stride).
+#ifndef BORIS_FUSED_GRID
+#define BORIS_FUSED_GRID 2
+#endif
+inline int64_t fused_grid(const void *kernel, int64_t work_blocks, int device) {
+    if (BORIS_FUSED_GRID == 0) return resident_grid(kernel, kFusedThreads, work_blocks, device);
+    if (BORIS_FUSED_GRID == 2) return work_blocks;
+    return stream_grid(work_blocks, 2048 / kFusedThreads, device);
+}
 
 template <typename FP>
 cudaError_t launch_stream_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,

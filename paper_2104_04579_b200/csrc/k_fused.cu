@@ -212,6 +212,82 @@ struct Particle {
     }
 };
 
+// m-dipole branch grouping.  Each block takes tiles of kMdGroup x kFusedThreads
+// particles; at the start of a launch the particles of a tile whose xi = kR is
+// below xi* (Taylor branch, reading c13) are assigned to the lowest thread slots,
+// the closed-form ones after them, so that at most one warp-round per tile runs
+// both branches (with one particle per thread in storage order, a 0.6-lambda
+// sphere puts a Taylor particle in ~87 % of warps, and a divergent warp executes
+// both bodies).  Scheduling only: every particle's arithmetic is unchanged, so
+// results are bitwise identical to the unpartitioned kernel; particles keep
+// their storage slots (c18).
+#ifndef BORIS_MD_GROUP
+#define BORIS_MD_GROUP 2
+#endif
+constexpr int kMdGroup = BORIS_MD_GROUP;
+
+// Fills s_slot[g * kFusedThreads + t] (g < kMdGroup) with the tile offsets of the
+// particles thread t pushes in round g (-1: none).  Contains two barriers; the
+// caller's loop over tiles must be block-uniform.
+template <typename FP, int LAYOUT>
+__device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArgs<FP> &fa,
+                                             int64_t base, int *s_slot, int *s_cnt) {
+    constexpr int W = kFusedThreads / 32, Q = kMdGroup * W;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned below = (1u << lane) - 1u;
+    unsigned bt[kMdGroup], bc[kMdGroup];
+#pragma unroll
+    for (int g = 0; g < kMdGroup; ++g) {
+        const int64_t i = base + g * kFusedThreads + threadIdx.x;
+        bool taylor = false;
+        if (i < e.n) {
+            FP x, y, z;
+            if constexpr (LAYOUT == BORIS_LAYOUT_SOA) {
+                x = ((const FP *)e.soa.x)[i];
+                y = ((const FP *)e.soa.y)[i];
+                z = ((const FP *)e.soa.z)[i];
+            } else {
+                const FP *r = (const FP *)((const unsigned char *)e.aos +
+                                           i * (sizeof(FP) == 4 ? 36 : 72));
+                x = r[0]; y = r[1]; z = r[2];
+            }
+            // the branch test of the first step (k_fused: x = (FP)xa + 0)
+            taylor = b_mul(fa.k, b_sqrt(b_norm2(x, y, z))) < MdBranch<FP>::xi_star;
+        }
+        bt[g] = __ballot_sync(0xffffffffu, i < e.n && taylor);
+        bc[g] = __ballot_sync(0xffffffffu, i < e.n && !taylor);
+        if (lane == 0) {
+            s_cnt[2 * (g * W + warp)] = __popc(bt[g]);
+            s_cnt[2 * (g * W + warp) + 1] = __popc(bc[g]);
+        }
+    }
+    __syncthreads();
+    int tot_t = 0, tot_c = 0, pre_t[kMdGroup], pre_c[kMdGroup];
+#pragma unroll
+    for (int g = 0; g < kMdGroup; ++g) pre_t[g] = pre_c[g] = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int ct = s_cnt[2 * q], cc = s_cnt[2 * q + 1];
+#pragma unroll
+        for (int g = 0; g < kMdGroup; ++g)
+            if (q < g * W + warp) {
+                pre_t[g] += ct;
+                pre_c[g] += cc;
+            }
+        tot_t += ct;
+        tot_c += cc;
+    }
+#pragma unroll
+    for (int g = 0; g < kMdGroup; ++g) {
+        const int off = g * kFusedThreads + threadIdx.x;
+        const unsigned me = 1u << lane;
+        if (bt[g] & me) s_slot[pre_t[g] + __popc(bt[g] & below)] = off;
+        if (bc[g] & me) s_slot[tot_t + pre_c[g] + __popc(bc[g] & below)] = off;
+        if (off >= tot_t + tot_c) s_slot[off] = -1;
+    }
+    __syncthreads();
+}
+
 }  // namespace
 
 // The fused step loop runs in windows of kFlush steps.  At each window start the
@@ -246,7 +322,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     }
     double ke = 0.0, cnt = 0.0;
     const int64_t stride = (int64_t)gridDim.x * kFusedThreads;
-    for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride) {
+    auto push_particle = [&](int64_t i) {
         double xa, ya, za;
         FP px, py, pz, w;
         int ty;
@@ -352,6 +428,23 @@ __global__ void __launch_bounds__(kFusedThreads)
             ke += (double)kinetic_energy<FP>(ux, uy, uz, gam, w, tc);
             cnt += 1.0;
         }
+    };
+    if constexpr (FIELD == FK_MDIPOLE && kMdGroup > 1) {
+        __shared__ int s_slot[kMdGroup * kFusedThreads];
+        __shared__ int s_cnt[2 * kMdGroup * (kFusedThreads / 32)];
+        const int64_t tile = (int64_t)kMdGroup * kFusedThreads;
+        for (int64_t base = (int64_t)blockIdx.x * tile; base < e.n;
+             base += (int64_t)gridDim.x * tile) {  // block-uniform
+            md_partition<FP, LAYOUT>(e, fa, base, s_slot, s_cnt);
+#pragma unroll 1
+            for (int g = 0; g < kMdGroup; ++g) {
+                const int off = s_slot[g * kFusedThreads + threadIdx.x];
+                if (off >= 0) push_particle(base + off);
+            }
+        }
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride)
+            push_particle(i);
     }
     if (DIAG) block_diag_partial<kFusedThreads>(ke, cnt, partials);
 }
@@ -360,19 +453,17 @@ template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER>
 static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
                                   const Coefs<FP> &co, int64_t n_steps, DiagOut *diag,
                                   int device, cudaStream_t st) {
-    const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
-    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads, device);
-    if (DIAG && grid > diag->cap) grid = diag->cap;
+    const int64_t per_block = FIELD == FK_MDIPOLE ? (int64_t)kMdGroup * kFusedThreads
+                                                  : (int64_t)kFusedThreads;
+    const int64_t blocks = (e.n + per_block - 1) / per_block;
     constexpr bool kHasYZ =
         (FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE) && PUSHER == PUSHER_BORIS;
-    if (kHasYZ && fa.yz)
-        k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, kHasYZ>
-            <<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, co, n_steps,
-                                                       diag ? diag->partials : nullptr);
-    else
-        k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, false>
-            <<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, co, n_steps,
-                                                       diag ? diag->partials : nullptr);
+    const auto kern = (kHasYZ && fa.yz) ? &k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, kHasYZ>
+                                        : &k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, false>;
+    int64_t grid = fused_grid((const void *)kern, blocks > 0 ? blocks : 1, device);
+    if (DIAG && grid > diag->cap) grid = diag->cap;
+    kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, co, n_steps,
+                                                  diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }

@@ -81,9 +81,10 @@ static cudaError_t dispatch_fa(const EnsView &e, const FieldSoaPtrs &f, const vo
                                const Coefs<FP> &co, int64_t n_steps, DiagOut *diag, int device,
                                cudaStream_t st) {
     const int64_t blocks = (e.n + kFusedThreads - 1) / kFusedThreads;
-    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kFusedThreads, device);
+    const auto kern = &k_fused_arrays<FP, LAYOUT, MULTI, DIAG, PUSHER>;
+    int64_t grid = fused_grid((const void *)kern, blocks > 0 ? blocks : 1, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    k_fused_arrays<FP, LAYOUT, MULTI, DIAG, PUSHER><<<(unsigned)grid, kFusedThreads, 0, st>>>(
+    kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(
         e, f, frec, co, n_steps, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();

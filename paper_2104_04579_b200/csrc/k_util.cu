@@ -65,6 +65,21 @@ int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device) {
     return work_blocks < cap ? work_blocks : cap;
 }
 
+int64_t resident_grid(const void *kernel, int threads, int64_t work_blocks, int device) {
+    // ALU-bound grid-stride kernels: exactly the blocks that are resident at once
+    // (occupancy of this instantiation), so every block starts in the first wave
+    // and all do the same work -- no partial tail wave.
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) !=
+            cudaSuccess ||
+        per_sm < 1) {
+        (void)cudaGetLastError();
+        per_sm = 1;
+    }
+    const int64_t cap = (int64_t)sm_count(device) * per_sm;
+    return work_blocks < cap ? work_blocks : cap;
+}
+
 // ---------------------------------------------------------------------------
 // Kinetic-energy diagnostic of the current state (reading c17).
 // ---------------------------------------------------------------------------

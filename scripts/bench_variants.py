@@ -127,10 +127,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--fused-only", action="store_true")
+    ap.add_argument("--mdipole-only", action="store_true")
     a = ap.parse_args()
     n1 = 10_000_000 if a.quick else 100_000_000
     three = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
     rows = []
+    if a.mdipole_only:
+        for layout in ("soa", "aos"):
+            rows.append(fused(f"mdipole-{layout}-fp32-100", "C4", layout, "fp32", n1 // 4, 100,
+                              field_kind="mdipole"))
+            rows.append(fused(f"mdipole-{layout}-fp64-100", "C4", layout, "fp64", n1 // 10, 100,
+                              field_kind="mdipole"))
+        for r in rows:
+            print(json.dumps(r), flush=True)
+        return
     for n in ([] if a.fused_only else [10_000_000] + ([n1] if n1 != 10_000_000 else [])):
         for layout in ("soa", "aos"):
             for prec in ("fp32", "fp64"):

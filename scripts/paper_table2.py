@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--n", type=int, default=10_000_000)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--only", default=None, help="run one scenario (precalc, precalc fused, "
+                                                  "analytic)")
     a = ap.parse_args()
     k = synth.OMEGA0 / synth.C_LIGHT
     A0 = k * math.sqrt(3.0 * 1e21 / synth.C_LIGHT)   # reading c12, P = 0.1 PW = 1e21 erg/s
@@ -66,6 +68,8 @@ def main():
             for scenario, flags in (("precalc", lb.BORIS_PUSH_STREAM_EACH_STEP),
                                     ("precalc fused", lb.BORIS_PUSH_AUTO),
                                     ("analytic", None)):
+                if a.only is not None and scenario != a.only:
+                    continue
                 ens.fill(d0)
                 ens.wrap()
                 if flags is not None:

@@ -348,6 +348,39 @@ def mdipole_workload():
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_mdipole_branch_grouping_is_scheduling_only(precision, layout):
+    """The fused m-dipole kernel regroups each tile's particles by radial branch
+    (k_fused.cu md_partition).  Pushing slices that start at offsets unrelated to
+    the tile size groups different particles together; results must not change."""
+    w = mdipole_workload()
+    n = 3 * 4096 + 37
+    d = rounded(w.generate(0, n), precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    field = gpu_field(w)
+    whole = cls(n, PREC[precision], w.types, w.light_velocity)
+    whole.fill(d)
+    whole.wrap()
+    lb.boris_push(whole.handle, field, w.dt, 40)
+    cuts = [0, 1001, 5003, 5004, n]
+    parts = []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        e = cls(hi - lo, PREC[precision], w.types, w.light_velocity)
+        e.fill({k: v[lo:hi] for k, v in d.items()})
+        e.wrap()
+        lb.boris_push(e.handle, field, w.dt, 40)
+        parts.append(e)
+    torch.cuda.synchronize()
+    ws = whole.state()
+    ps = [p.state() for p in parts]
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(torch.cat([s[k] for s in ps]), ws[k]), k
+    for e in parts + [whole]:
+        e.close()
+    lb.boris_field_destroy(field)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_mdipole_parity(precision):
     w = mdipole_workload()
     worst = run_parity(w, "soa", precision, N_SMALL, checks=(1, 2, 10, 100))
