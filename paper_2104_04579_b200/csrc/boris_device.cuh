@@ -178,14 +178,16 @@ __device__ __forceinline__ FP boris_momentum_yz(FP &ux, FP &uy, FP &uz, FP c, FP
 }
 
 // One Boris momentum update on the scaled momentum u (steps a4-a9).
-// Returns 1/gamma^{n+1/2}; writes gamma^{n+1/2} to `gamma`.
-template <typename FP>
+// Returns 1/gamma^{n+1/2}; writes gamma^{n+1/2} to `gamma`.  EZ0: the caller's
+// E_z is exactly zero (the m-dipole, eq. 14), so the z kicks u_z + aE 0 are
+// skipped -- the same value up to the sign of a zero u_z.
+template <typename FP, bool EZ0 = false>
 __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP Ey, FP Ez, FP Bx,
                                              FP By, FP Bz, const TypeCoef<FP> &tc, FP &gamma) {
     // a4: first electric half kick (eq. 9), u + aE E as one FMA per component
     ux = b_fma(tc.aE, Ex, ux);
     uy = b_fma(tc.aE, Ey, uy);
-    uz = b_fma(tc.aE, Ez, uz);
+    if (!EZ0) uz = b_fma(tc.aE, Ez, uz);
     // a5: 1/gamma_n, gamma_n = gamma(u^-) (L162, reading c2)
     const FP inv_gn = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
     // a6: rotation vectors (eq. 13)
@@ -195,7 +197,7 @@ __device__ __forceinline__ FP boris_momentum(FP &ux, FP &uy, FP &uz, FP Ex, FP E
     // a8: second electric half kick (eq. 10)
     ux = b_fma(tc.aE, Ex, ux);
     uy = b_fma(tc.aE, Ey, uy);
-    uz = b_fma(tc.aE, Ez, uz);
+    if (!EZ0) uz = b_fma(tc.aE, Ez, uz);
     // a9: gamma^{n+1/2} (eq. 5, reading c3) and its reciprocal
     return boris_gamma<FP>(ux, uy, uz, tc.kappa2, gamma);
 }

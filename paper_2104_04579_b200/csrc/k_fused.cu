@@ -89,6 +89,18 @@ struct MdBranch<float> {  // reading c13: fp32 xi* = 1.5, 7 terms
     static constexpr int terms = 7;
 };
 
+// R = |r| for the m-dipole: fp32 R2 rsqrt(R2) with the MUFU rsqrt (<= 2 ulp, like
+// every other fp32 square root of the push; R = 0 at the origin) unless
+// BORIS_PRECISE_MATH; fp64 correctly rounded.
+__device__ __forceinline__ float md_radius(float r2) {
+#ifdef BORIS_PRECISE_MATH
+    return __fsqrt_rn(r2);
+#else
+    return r2 > 0.f ? b_mul(r2, b_rsqrt(r2)) : 0.f;
+#endif
+}
+__device__ __forceinline__ double md_radius(double r2) { return __dsqrt_rn(r2); }
+
 template <typename FP>
 __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
     if (xi < MdBranch<FP>::xi_star) {
@@ -252,7 +264,7 @@ __device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArg
                 x = r[0]; y = r[1]; z = r[2];
             }
             // the branch test of the first step (k_fused: x = (FP)xa + 0)
-            taylor = b_mul(fa.k, b_sqrt(b_norm2(x, y, z))) < MdBranch<FP>::xi_star;
+            taylor = b_mul(fa.k, md_radius(b_norm2(x, y, z))) < MdBranch<FP>::xi_star;
         }
         bt[g] = __ballot_sync(0xffffffffu, i < e.n && taylor);
         bc[g] = __ballot_sync(0xffffffffu, i < e.n && !taylor);
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
-                    const FP R = b_sqrt(b_norm2(x, y, z));
+                    const FP R = md_radius(b_norm2(x, y, z));
                     FP g1, g2, f3;
                     md_radial<FP>(b_mul(fa.k, R), g1, g2, f3);
                     const FP swt = s_sin[s0 + j], cwt = s_cos[s0 + j];
@@ -399,7 +411,12 @@ __global__ void __launch_bounds__(kFusedThreads)
                     Bx = b_mul(b_mul(sk, x), z);
                     By = b_mul(b_mul(sk, y), z);
                     Bz = b_mul(sb, b_fma(k2g2, b_mul(z, z), f3));
-                    inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
+                    if constexpr (PUSHER == PUSHER_BORIS)  // E_z = 0 exactly (eq. 14)
+                        inv_g = boris_momentum<FP, true>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc,
+                                                         gam);
+                    else
+                        inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz,
+                                                            tc, gam);
                 }
                 // a10 (eq. 7): displacement accumulated in the window
                 const FP ct = b_mul(tc.cr, inv_g);
