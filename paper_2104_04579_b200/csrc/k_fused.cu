@@ -309,7 +309,17 @@ __device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArg
 // and reduced mod 2 pi; inside the window
 //   phi_n = phi_a + kvec . (r - r_a) - (n - n_a) omega dt      (FP, |.| <~ pi + 0.5)
 // which is phi = k (k_hat . r^n) - omega t_n + phase0 (reading c5) re-associated.
-constexpr int kFlush = 8;
+// Window length: fp32 16 steps (8: C4 1.287 ps, 12: 1.217, 16: 1.181 per particle-step;
+// parity after 100 steps 4.2e-6 -> 5.2e-6 of the 1e-5 bar, profiles/r01/exp_flush_window/),
+// fp64 8 (16 spills in the alternative pushers and is slower).
+#ifndef BORIS_FUSED_FLUSH32
+#define BORIS_FUSED_FLUSH32 16
+#endif
+#ifndef BORIS_FUSED_FLUSH64
+#define BORIS_FUSED_FLUSH64 8
+#endif
+template <typename FP>
+constexpr int kFlushOf = sizeof(FP) == 4 ? BORIS_FUSED_FLUSH32 : BORIS_FUSED_FLUSH64;
 // m-dipole: sin/cos(omega0 t_n) is the same for every particle; each block
 // tabulates it (fp64 sincos, cast to FP) once per launch in shared memory.
 // Launches are split into chunks of kTimeTab steps on the host.
@@ -319,6 +329,7 @@ template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER,
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
+    constexpr int kFlush = kFlushOf<FP>;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     __shared__ FP s_sin[FIELD == FK_MDIPOLE ? kTimeTab : 1];
     __shared__ FP s_cos[FIELD == FK_MDIPOLE ? kTimeTab : 1];
