@@ -177,6 +177,76 @@ __device__ __forceinline__ FP boris_momentum_yz(FP &ux, FP &uy, FP &uz, FP c, FP
     return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
 }
 
+// Merged-reciprocal variants of boris_momentum_dir / _yz (register-fused kernels).
+// With tau = alpha B (= c ab) and g2 = gamma_n^2, D = g2 + |tau|^2:
+//   t = tau / gamma_n,  s = 2 t / (1 + |t|^2) = 2 tau gamma_n / D,
+// and both come from ONE reciprocal square root r = rsqrt(g2 D^2) = 1/(gamma_n D):
+//   t = (D r) tau,  s = (2 g2 r) tau,
+// instead of rsqrt(g2) and the reciprocal 1/(1 + |t|^2) (eq. 13 re-associated).  The
+// operands are pre-scaled by powers of two (exact): g2s = 2^-32 g2 (kappa2s =
+// 2^-32 kappa2, ones = 2^-32), taus = 2^-16 tau (abs = 2^-16 ab), taus2 = 2^-15 tau
+// (abs2), so X = g2s Ds^2 = 2^-96 g2 D^2 stays a normal fp32 number for
+// 1 <= gamma_n, |tau| < 2^37; then Ds r = 2^16/gamma_n and g2s r = 2^16 gamma_n/D.
+template <typename FP>
+__device__ __forceinline__ void boris_rotate_ts(FP &ux, FP &uy, FP &uz, FP tx, FP ty, FP tz,
+                                                FP sx, FP sy, FP sz) {
+    const FP upx = b_fma(uy, tz, b_fma(-uz, ty, ux));
+    const FP upy = b_fma(uz, tx, b_fma(-ux, tz, uy));
+    const FP upz = b_fma(ux, ty, b_fma(-uy, tx, uz));
+    ux = b_fma(upy, sz, b_fma(-upz, sy, ux));
+    uy = b_fma(upz, sx, b_fma(-upx, sz, uy));
+    uz = b_fma(upx, sy, b_fma(-upy, sx, uz));
+}
+
+template <typename FP, bool UNIT>
+__device__ __forceinline__ FP boris_momentum_dir_m(FP &ux, FP &uy, FP &uz, FP c,
+                                                   const FP (&ae)[3], const FP (&abs)[3],
+                                                   const FP (&abs2)[3], FP kappa2, FP kappa2s,
+                                                   FP ones, FP &gamma) {
+    auto kick = [&](FP u, FP a) { return UNIT ? b_add(u, a) : b_fma(c, a, u); };
+    ux = kick(ux, ae[0]);
+    uy = kick(uy, ae[1]);
+    uz = kick(uz, ae[2]);
+    const FP g2s = b_fma(kappa2s, b_norm2(ux, uy, uz), ones);
+    FP ts[3], ts2[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        ts[k] = UNIT ? abs[k] : b_mul(c, abs[k]);
+        ts2[k] = UNIT ? abs2[k] : b_mul(c, abs2[k]);
+    }
+    const FP Ds = b_fma(ts[0], ts[0], b_fma(ts[1], ts[1], b_fma(ts[2], ts[2], g2s)));
+    const FP r = b_rsqrt(b_mul(b_mul(g2s, Ds), Ds));
+    const FP ft = b_mul(Ds, r), fs = b_mul(g2s, r);
+    boris_rotate_ts<FP>(ux, uy, uz, b_mul(ft, ts[0]), b_mul(ft, ts[1]), b_mul(ft, ts[2]),
+                        b_mul(fs, ts2[0]), b_mul(fs, ts2[1]), b_mul(fs, ts2[2]));
+    ux = kick(ux, ae[0]);
+    uy = kick(uy, ae[1]);
+    uz = kick(uz, ae[2]);
+    return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
+}
+
+// boris_momentum_dir_m for E || y^, B || z^: the same roundings with the exact
+// zeros dropped (fma(0, 0, x) == x), bitwise identical.
+template <typename FP, bool UNIT>
+__device__ __forceinline__ FP boris_momentum_yz_m(FP &ux, FP &uy, FP &uz, FP c, FP aey, FP absz,
+                                                  FP abs2z, FP kappa2, FP kappa2s, FP ones,
+                                                  FP &gamma) {
+    uy = UNIT ? b_add(uy, aey) : b_fma(c, aey, uy);
+    const FP g2s = b_fma(kappa2s, b_norm2(ux, uy, uz), ones);
+    const FP ts = UNIT ? absz : b_mul(c, absz);
+    const FP ts2 = UNIT ? abs2z : b_mul(c, abs2z);
+    const FP Ds = b_fma(ts, ts, g2s);
+    const FP r = b_rsqrt(b_mul(b_mul(g2s, Ds), Ds));
+    const FP tz = b_mul(b_mul(Ds, r), ts);
+    const FP sz = b_mul(b_mul(g2s, r), ts2);
+    const FP upx = b_fma(uy, tz, ux);
+    const FP upy = b_fma(-ux, tz, uy);
+    ux = b_fma(upy, sz, ux);
+    uy = b_fma(-upx, sz, uy);
+    uy = UNIT ? b_add(uy, aey) : b_fma(c, aey, uy);
+    return boris_gamma<FP>(ux, uy, uz, kappa2, gamma);
+}
+
 // One Boris momentum update on the scaled momentum u (steps a4-a9).
 // Returns 1/gamma^{n+1/2}; writes gamma^{n+1/2} to `gamma`.  EZ0: the caller's
 // E_z is exactly zero (the m-dipole, eq. 14), so the z kicks u_z + aE 0 are

@@ -318,6 +318,19 @@ __device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArg
 #ifndef BORIS_FUSED_FLUSH64
 #define BORIS_FUSED_FLUSH64 8
 #endif
+// One reciprocal square root for t and s (boris_momentum_*_m): measured 10 % faster
+// on the fp64 uniform-field kernel (C3), slower on fp32 and on the generic-orientation
+// plane wave (profiles/r01/exp_merged_rsqrt/).  BORIS_MERGED_RSQRT (tuning): 0 never,
+// 1 every uniform / plane-wave Boris kernel, 2 fp64 uniform fields only.
+#ifndef BORIS_MERGED_RSQRT
+#define BORIS_MERGED_RSQRT 2
+#endif
+template <typename FP, int FIELD>
+constexpr bool kMergedRsqrt =
+    (FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE) &&
+    (BORIS_MERGED_RSQRT == 1 ||
+     (BORIS_MERGED_RSQRT == 2 && sizeof(FP) == 8 && FIELD == FK_UNIFORM));
+
 template <typename FP>
 constexpr int kFlushOf = sizeof(FP) == 4 ? BORIS_FUSED_FLUSH32 : BORIS_FUSED_FLUSH64;
 // m-dipole: sin/cos(omega0 t_n) is the same for every particle; each block
@@ -330,6 +343,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
     constexpr int kFlush = kFlushOf<FP>;
+    constexpr bool kMerged = kMergedRsqrt<FP, FIELD>;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     __shared__ FP s_sin[FIELD == FK_MDIPOLE ? kTimeTab : 1];
     __shared__ FP s_cos[FIELD == FK_MDIPOLE ? kTimeTab : 1];
@@ -365,6 +379,17 @@ __global__ void __launch_bounds__(kFusedThreads)
                 ab[k] = b_mul(tc.alpha, bv[k]);
             }
         }
+        // boris_momentum_*_m operands (exact power-of-two scalings)
+        FP abs_[3] = {FP(0), FP(0), FP(0)}, abs2[3] = {FP(0), FP(0), FP(0)};
+        if constexpr (kMerged) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                abs_[k] = b_mul(ab[k], FP(1.52587890625e-05));  // 2^-16
+                abs2[k] = b_mul(ab[k], FP(3.0517578125e-05));   // 2^-15
+            }
+        }
+        const FP kappa2s = b_mul(tc.kappa2, FP(2.3283064365386963e-10));  // 2^-32
+        const FP ones = FP(2.3283064365386963e-10);
         for (int64_t s0 = 0; s0 < n_steps; s0 += kFlush) {
             FP phia = FP(0);
             if constexpr (FIELD == FK_PLANE_WAVE)
@@ -375,7 +400,14 @@ __global__ void __launch_bounds__(kFusedThreads)
             auto step = [&](int j) {
                 FP inv_g;
                 if constexpr (FIELD == FK_UNIFORM) {
-                    if constexpr (YZ)
+                    if constexpr (kMerged && YZ)
+                        inv_g = boris_momentum_yz_m<FP, true>(ux, uy, uz, FP(1), ae[1], abs_[2],
+                                                              abs2[2], tc.kappa2, kappa2s, ones,
+                                                              gam);
+                    else if constexpr (kMerged && PUSHER == PUSHER_BORIS)
+                        inv_g = boris_momentum_dir_m<FP, true>(ux, uy, uz, FP(1), ae, abs_, abs2,
+                                                               tc.kappa2, kappa2s, ones, gam);
+                    else if constexpr (YZ)
                         inv_g = boris_momentum_yz<FP, true>(ux, uy, uz, FP(1), ae[1], ab[2],
                                                             tc.kappa2, gam);
                     else if constexpr (PUSHER == PUSHER_BORIS)
@@ -390,7 +422,14 @@ __global__ void __launch_bounds__(kFusedThreads)
                                       : b_fma(fa.kf[0], dx, b_fma(fa.kf[1], dy, b_fma(fa.kf[2], dz,
                                         b_fma(-(FP)j, fa.wdtf, phia))));
                     const FP c = cos_small(phi);  // E = E0 e_hat c, B = E0 (k_hat x e_hat) c
-                    if constexpr (YZ)
+                    if constexpr (kMerged && YZ)
+                        inv_g = boris_momentum_yz_m<FP, false>(ux, uy, uz, c, ae[1], abs_[2],
+                                                               abs2[2], tc.kappa2, kappa2s, ones,
+                                                               gam);
+                    else if constexpr (kMerged && PUSHER == PUSHER_BORIS)
+                        inv_g = boris_momentum_dir_m<FP, false>(ux, uy, uz, c, ae, abs_, abs2,
+                                                                tc.kappa2, kappa2s, ones, gam);
+                    else if constexpr (YZ)
                         inv_g = boris_momentum_yz<FP, false>(ux, uy, uz, c, ae[1], ab[2],
                                                              tc.kappa2, gam);
                     else if constexpr (PUSHER == PUSHER_BORIS)
