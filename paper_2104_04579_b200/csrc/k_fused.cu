@@ -133,7 +133,7 @@ __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
 #endif
         } else {
             sincos(xi, &sn, &cs);
-            ix = FP(1) / xi;
+            ix = __drcp_rn(xi);  // == 1.0 / xi (both correctly rounded), no division
         }
         const FP ix2 = ix * ix, ix3 = ix2 * ix;
         const FP f1 = sn * ix2 - cs * ix;
@@ -309,6 +309,12 @@ __device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArg
 // and reduced mod 2 pi; inside the window
 //   phi_n = phi_a + kvec . (r - r_a) - (n - n_a) omega dt      (FP, |.| <~ pi + 0.5)
 // which is phi = k (k_hat . r^n) - omega t_n + phase0 (reading c5) re-associated.
+// Grid field in the fused kernel: keep the particle's cell records in registers
+// across steps (grid_gather_cached); 0 gathers every step from L1/L2.
+#ifndef BORIS_GRID_CACHE
+#define BORIS_GRID_CACHE 1
+#endif
+
 // Window length: fp32 16 steps (8: C4 1.287 ps, 12: 1.217, 16: 1.181 per particle-step;
 // parity after 100 steps 4.2e-6 -> 5.2e-6 of the 1e-5 bar, profiles/r01/exp_flush_window/),
 // fp64 8 (16 spills in the alternative pushers and is slower).
@@ -390,6 +396,9 @@ __global__ void __launch_bounds__(kFusedThreads)
         }
         const FP kappa2s = b_mul(tc.kappa2, FP(2.3283064365386963e-10));  // 2^-32
         const FP ones = FP(2.3283064365386963e-10);
+#if BORIS_GRID_CACHE
+        GridCache<FP> gcache;  // FK_GRID: the particle's cell records (dead code otherwise)
+#endif
         for (int64_t s0 = 0; s0 < n_steps; s0 += kFlush) {
             FP phia = FP(0);
             if constexpr (FIELD == FK_PLANE_WAVE)
@@ -441,8 +450,13 @@ __global__ void __launch_bounds__(kFusedThreads)
                             b_mul(fa.cB[0], c), b_mul(fa.cB[1], c), b_mul(fa.cB[2], c), tc, gam);
                 } else if constexpr (FIELD == FK_GRID) {  // CIC gather (reading c-grid)
                     FP Ex, Ey, Ez, Bx, By, Bz;
+#if BORIS_GRID_CACHE
+                    grid_gather_cached<FP>(fa.grid, b_add((FP)xa, dx), b_add((FP)ya, dy),
+                                           b_add((FP)za, dz), gcache, Ex, Ey, Ez, Bx, By, Bz);
+#else
                     grid_gather<FP>(fa.grid, b_add((FP)xa, dx), b_add((FP)ya, dy),
                                     b_add((FP)za, dz), Ex, Ey, Ez, Bx, By, Bz);
+#endif
                     inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
