@@ -116,9 +116,6 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
 #ifndef BORIS_GRID_MINB
 #define BORIS_GRID_MINB 3
 #endif
-#ifndef BORIS_GRID_STREAM_CACHE
-#define BORIS_GRID_STREAM_CACHE 0
-#endif
 #define BORIS_GRID_BOUNDS __launch_bounds__(kStreamThreads, BORIS_GRID_MINB)
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void BORIS_GRID_BOUNDS
@@ -153,19 +150,9 @@ __global__ void BORIS_GRID_BOUNDS
             }
         }
         FP ex[V], ey[V], ez[V], bx[V], by[V], bz[V];
-#if BORIS_GRID_STREAM_CACHE
-        // the V consecutive particles of a thread share their cell when sorted:
-        // reload the cell records only on a cell change (grid_gather_cached)
-        GridCache<FP> gcache;
-#pragma unroll
-        for (int j = 0; j < V; ++j)
-            grid_gather_cached<FP>(g, x.v[j], y.v[j], z.v[j], gcache, ex[j], ey[j], ez[j], bx[j],
-                                   by[j], bz[j]);
-#else
 #pragma unroll
         for (int j = 0; j < V; ++j)
             grid_gather<FP>(g, x.v[j], y.v[j], z.v[j], ex[j], ey[j], ez[j], bx[j], by[j], bz[j]);
-#endif
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const TypeCoef<FP> tc = MULTI ? s_t[ty[j]] : co.t[0];
