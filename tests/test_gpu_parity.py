@@ -789,6 +789,35 @@ def test_grid_push_parity(precision):
     ens.close()
 
 
+def test_grid_fused_push_with_frequent_cell_crossings():
+    """The fused grid kernel keeps a particle's cell records in registers and reloads
+    them on a cell change (grid.cuh grid_gather_cached).  A fine grid and a larger dt
+    make most particles cross several cells within one 100-step launch; fp64 parity
+    with the oracle must hold through the reloads."""
+    precision = "fp64"
+    h, params, gE, gB = grid_setup(precision, nx=96, ny=80, nz=64)
+    w = synth.config("C2")
+    w.dt = synth.T0 / 2000.0
+    d, ens, field = build(w, "soa", precision, N_SMALL)
+    ref = OracleRun(w, d, precision)
+    ref.kind, ref.params, ref.E, ref.B = oracle.FIELD_GRID, params, gE, gB
+    lb.boris_push(ens.handle, h, w.dt, 100)
+    ref.push(100)
+    torch.cuda.synchronize()
+    r, p, g, st = gpu_state(ens)
+    metric = C15()
+    er, ep = metric("r", r, ref.pos), metric("p", p, ref.mom)
+    assert er <= TOL[precision] and ep <= TOL[precision], (er, ep)
+    # non-vacuous: most particles changed cell during the launch
+    org, hs = np.array(params[0:3]), np.array(params[3:6])
+    c0 = np.floor((stack3(d, "x", "y", "z") - org) / hs)
+    c1 = np.floor((ref.pos - org) / hs)
+    moved = np.mean(np.any(c0 != c1, axis=1))
+    assert moved > 0.5, moved
+    lb.boris_field_destroy(h)
+    ens.close()
+
+
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("layout", ["soa", "aos"])
 def test_sort_by_cell_is_a_stable_permutation(precision, layout):
