@@ -8,6 +8,8 @@
 // thread and a warp touches 512 contiguous bytes per array; all loads of a
 // group are issued before any arithmetic (12 x LDG.128 in flight per thread).
 // Grid-stride over groups with a grid sized to the resident-block count.
+#include <stdlib.h>
+
 #include "boris_internal.h"
 #include "deposit.cuh"
 
@@ -439,6 +441,18 @@ __global__ void __launch_bounds__(kStreamThreads)
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
+// Tuning: BORIS_STREAM_GRID=<blocks> overrides the grid of the vector streaming
+// kernel (experiments on grid size under the board power cap; 0/unset: default).
+static int64_t stream_grid_override() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *s = getenv("BORIS_STREAM_GRID");
+        v = s ? atoll(s) : 0;
+        if (v < 0) v = 0;
+    }
+    return v;
+}
+
 template <typename FP, bool MULTI, bool DIAG>
 static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
                                 DiagOut *diag, int device, cudaStream_t st) {
@@ -455,6 +469,8 @@ static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const C
         const int64_t n_groups = e.n / V;
         const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
         grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+        if (stream_grid_override() > 0 && stream_grid_override() < grid)
+            grid = stream_grid_override();
         if (DIAG && grid > diag->cap) grid = diag->cap;
         k_stream_soa_vec<FP, MULTI, DIAG>
             <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, co, n_groups, e.n, partials);
