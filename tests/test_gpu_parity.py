@@ -694,6 +694,44 @@ def test_full_size_C5_bench_configuration():
     ens.close()
 
 
+def test_beyond_int32_particle_indices():
+    """n = 2^31 + 37 (the C5 recipe; ~125 GB of HBM): every index is 64-bit in the
+    streaming kernel, the fused KE reduction and the ragged tail.  Sampled particles
+    around 2^31 and at the end vs the oracle; the diagnostic count is exact."""
+    free, _ = torch.cuda.mem_get_info()
+    n = (1 << 31) + 37
+    if free < 140e9:
+        pytest.skip(f"needs ~125 GB of free device memory, {free / 1e9:.0f} GB free")
+    w = synth.config("C5", n=n)
+    ens = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity)
+    chunk = 1 << 25
+    for c0 in range(0, n, chunk):
+        ens.fill(w.generate(c0, min(chunk, n - c0), device="cuda"), first=c0)
+    ens.wrap()
+    b = 1 << 31
+    idx = np.unique(np.r_[np.linspace(0, n - 1, 4000).astype(np.int64),
+                          np.arange(b - 40, min(n, b + 40)), np.arange(n - 40, n)])
+    ds = rounded(w.generate_indices(torch.from_numpy(idx)), "fp32")
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(ens.handle, ens.field, w.dt, 1, diag.data_ptr())
+    torch.cuda.synchronize()
+    assert diag[1].item() == n
+    ref = OracleRun(w, ds, "fp32")
+    ref.push(1)
+
+    def gather(t):
+        return np.array([t[int(i)].item() for i in idx], dtype=np.float64)
+
+    r = np.stack([gather(ens.t[k]) for k in ("x", "y", "z")], 1)
+    p = np.stack([gather(ens.t[k]) for k in ("px", "py", "pz")], 1)
+    metric = C15()
+    assert metric("r", r, ref.pos) <= TOL["fp32"]
+    assert metric("p", p, ref.mom) <= TOL["fp32"]
+    ens.close()
+    del ens
+    torch.cuda.empty_cache()
+
+
 def test_full_size_C2_fp32_soa_sampled():
     print(_sampled_full_size("C2", "soa", "fp32", 1))
 
