@@ -732,6 +732,79 @@ def test_beyond_int32_particle_indices():
     torch.cuda.empty_cache()
 
 
+def _big_sample(n):
+    b = 1 << 31
+    return np.unique(np.r_[np.linspace(0, n - 1, 3000).astype(np.int64),
+                           np.arange(b - 40, min(n, b + 40)), np.arange(n - 40, n)])
+
+
+def test_beyond_int32_aos_streaming():
+    """AoS (TMA record tiles) with 2^31 + 37 particles and per-particle field records
+    (~129 GB): 64-bit record offsets in the tile loop, the tail and the KE count."""
+    free, _ = torch.cuda.mem_get_info()
+    n = (1 << 31) + 37
+    if free < 145e9:
+        pytest.skip(f"needs ~130 GB of free device memory, {free / 1e9:.0f} GB free")
+    w = synth.config("C5", n=n)
+    ens = AosEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity)
+    chunk = 1 << 25
+    for c0 in range(0, n, chunk):
+        ens.fill(w.generate(c0, min(chunk, n - c0), device="cuda"), first=c0)
+    ens.wrap()
+    idx = _big_sample(n)
+    ds = rounded(w.generate_indices(torch.from_numpy(idx)), "fp32")
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(ens.handle, ens.field, w.dt, 1, diag.data_ptr())
+    torch.cuda.synchronize()
+    assert diag[1].item() == n
+    ref = OracleRun(w, ds, "fp32")
+    ref.push(1)
+    rec = np.array([ens.rec[int(i), :6].tolist() for i in idx], dtype=np.float64)
+    metric = C15()
+    assert metric("r", rec[:, :3], ref.pos) <= TOL["fp32"]
+    assert metric("p", rec[:, 3:6], ref.mom) <= TOL["fp32"]
+    ens.close()
+    del ens
+    torch.cuda.empty_cache()
+
+
+def test_beyond_int32_fused_multitype_uniform():
+    """The register-fused kernel (C3 recipe: three types, crossed uniform E x B, SoA
+    fp32, 10 fused steps) with 2^31 + 37 particles (~73 GB): one block per 128
+    particles is a 16.8M-block grid."""
+    free, _ = torch.cuda.mem_get_info()
+    n = (1 << 31) + 37
+    if free < 90e9:
+        pytest.skip(f"needs ~75 GB of free device memory, {free / 1e9:.0f} GB free")
+    w = synth.config("C3", n=n)
+    ens = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity, with_fields=False)
+    chunk = 1 << 25
+    for c0 in range(0, n, chunk):
+        ens.fill(w.generate(c0, min(chunk, n - c0), device="cuda"), first=c0)
+    ens.wrap()
+    field = gpu_field(w)
+    idx = _big_sample(n)
+    ds = rounded(w.generate_indices(torch.from_numpy(idx)), "fp32")
+    lb.boris_push(ens.handle, field, w.dt, 10)
+    torch.cuda.synchronize()
+    ref = OracleRun(w, ds, "fp32")
+    ref.push(10)
+
+    def gather(t):
+        return np.array([t[int(i)].item() for i in idx], dtype=np.float64)
+
+    r = np.stack([gather(ens.t[k]) for k in ("x", "y", "z")], 1)
+    p = np.stack([gather(ens.t[k]) for k in ("px", "py", "pz")], 1)
+    assert np.array_equal(gather(ens.t["type"]), ds["type"].numpy().astype(np.float64))
+    metric = C15()
+    assert metric("r", r, ref.pos) <= TOL["fp32"]
+    assert metric("p", p, ref.mom) <= TOL["fp32"]
+    lb.boris_field_destroy(field)
+    ens.close()
+    del ens
+    torch.cuda.empty_cache()
+
+
 def test_full_size_C2_fp32_soa_sampled():
     print(_sampled_full_size("C2", "soa", "fp32", 1))
 
