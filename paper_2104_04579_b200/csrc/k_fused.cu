@@ -340,7 +340,8 @@ constexpr bool kMergedRsqrt =
 template <typename FP>
 constexpr int kFlushOf = sizeof(FP) == 4 ? BORIS_FUSED_FLUSH32 : BORIS_FUSED_FLUSH64;
 // m-dipole: sin/cos(omega0 t_n) is the same for every particle; each block
-// tabulates it (fp64 sincos, cast to FP) once per launch in shared memory.
+// tabulates -2 A0 sin and 2 A0 k cos of it (fp64 sincos, cast to FP, times the FP
+// amplitude: the roundings the step would do) once per launch in shared memory.
 // Launches are split into chunks of kTimeTab steps on the host.
 constexpr int kTimeTab = 1024;
 
@@ -358,8 +359,8 @@ __global__ void __launch_bounds__(kFusedThreads)
         for (int j = threadIdx.x; j < n_steps; j += kFusedThreads) {
             double sn, cs;
             sincos(fa.w0t0 + (double)j * fa.w0dt, &sn, &cs);  // t_j = t0 + j dt (c5)
-            s_sin[j] = (FP)sn;
-            s_cos[j] = (FP)cs;
+            s_sin[j] = b_mul(fa.mA02, (FP)sn);   // -2 A0 sin(w t_j)
+            s_cos[j] = b_mul(fa.A0k2, (FP)cs);   // 2 A0 k cos(w t_j)
         }
         __syncthreads();
     }
@@ -464,9 +465,9 @@ __global__ void __launch_bounds__(kFusedThreads)
                     const FP R = md_radius(b_norm2(x, y, z));
                     FP g1, g2, f3;
                     md_radial<FP>(b_mul(fa.k, R), g1, g2, f3);
-                    const FP swt = s_sin[s0 + j], cwt = s_cos[s0 + j];
-                    const FP ce = b_mul(b_mul(fa.A0k2, cwt), g1);  // 2 A0 k cos(w t) f1/xi
-                    const FP sb = b_mul(fa.mA02, swt);              // -2 A0 sin(w t)
+                    // per-block tables hold the amplitudes (same roundings as in the step)
+                    const FP ce = b_mul(s_cos[s0 + j], g1);  // 2 A0 k cos(w t) f1/xi
+                    const FP sb = s_sin[s0 + j];             // -2 A0 sin(w t)
                     const FP k2g2 = b_mul(fa.k2, g2);               // f2/R^2
                     Ex = -b_mul(ce, y);
                     Ey = b_mul(ce, x);
