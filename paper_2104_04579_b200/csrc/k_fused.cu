@@ -144,6 +144,59 @@ __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
     }
 }
 
+// The radial functions from r^2 = |r|^2 (both callers: the fused step and the branch
+// grouping).  fp32 (default math) works with xi^2 = k^2 r^2: the Taylor branch is a
+// series in xi^2 (no square root), and the closed form takes 1/xi = rsqrt(xi^2) from
+// one MUFU rsqrt and xi = xi^2 / xi -- one MUFU fewer than R = sqrt(r^2), xi = k R,
+// 1/xi = rcp(xi); the branch test xi < 1.5 becomes xi^2 < 2.25 (reading c13).  fp64
+// (and BORIS_PRECISE_MATH) use R = sqrt(r^2), xi = k R.
+template <typename FP>
+__device__ __forceinline__ bool md_taylor(const AnalyticArgs<FP> &fa, FP r2) {
+#ifndef BORIS_PRECISE_MATH
+    if constexpr (sizeof(FP) == 4)
+        return b_mul(fa.k2, r2) < MdBranch<FP>::xi_star * MdBranch<FP>::xi_star;
+#endif
+    return b_mul(fa.k, md_radius(r2)) < MdBranch<FP>::xi_star;
+}
+template <typename FP>
+__device__ __forceinline__ void md_radial_r2(const AnalyticArgs<FP> &fa, FP r2, FP &g1, FP &g2,
+                                             FP &f3) {
+#ifndef BORIS_PRECISE_MATH
+    if constexpr (sizeof(FP) == 4) {
+        const float x2 = b_mul(fa.k2, r2);
+        if (x2 < MdBranch<float>::xi_star * MdBranch<float>::xi_star) {
+            constexpr int T = MdBranch<float>::terms;
+            float j0 = float(c_md.j0[T - 1]), j1x = float(c_md.j1x[T - 1]),
+                  s2 = float(c_md.g2[T - 1]);
+#pragma unroll
+            for (int n = T - 2; n >= 0; --n) {
+                j0 = j0 * x2 + float(c_md.j0[n]);
+                j1x = j1x * x2 + float(c_md.j1x[n]);
+            }
+#pragma unroll
+            for (int n = T - 2; n >= 1; --n) s2 = s2 * x2 + float(c_md.g2[n]);
+            g1 = j1x;
+            g2 = s2;
+            f3 = j0 - j1x;
+        } else {
+            const float ix = b_rsqrt(x2), xi = b_mul(x2, ix);
+            const float q = rintf(xi * 0.15915494f);
+            const float r = __fmaf_rn(-q, -1.7484555e-07f, __fmaf_rn(-q, 6.2831855f, xi));
+            float sn, cs;
+            __sincosf(r, &sn, &cs);
+            const float ix2 = ix * ix, ix3 = ix2 * ix;
+            const float f1 = sn * ix2 - cs * ix;
+            const float f2 = (3.f * ix3 - ix) * sn - 3.f * cs * ix2;
+            f3 = (ix - ix3) * sn + cs * ix2;
+            g1 = f1 * ix;
+            g2 = f2 * ix2;
+        }
+        return;
+    }
+#endif
+    md_radial<FP>(b_mul(fa.k, md_radius(r2)), g1, g2, f3);
+}
+
 template <typename FP, int FIELD>
 __device__ __forceinline__ void analytic_field(const AnalyticArgs<FP> &fa, double rx, double ry,
                                                double rz, int64_t n, FP &Ex, FP &Ey, FP &Ez,
@@ -264,7 +317,7 @@ __device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArg
                 x = r[0]; y = r[1]; z = r[2];
             }
             // the branch test of the first step (k_fused: x = (FP)xa + 0)
-            taylor = b_mul(fa.k, md_radius(b_norm2(x, y, z))) < MdBranch<FP>::xi_star;
+            taylor = md_taylor<FP>(fa, b_norm2(x, y, z));
         }
         bt[g] = __ballot_sync(0xffffffffu, i < e.n && taylor);
         bc[g] = __ballot_sync(0xffffffffu, i < e.n && !taylor);
@@ -462,9 +515,8 @@ __global__ void __launch_bounds__(kFusedThreads)
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
-                    const FP R = md_radius(b_norm2(x, y, z));
                     FP g1, g2, f3;
-                    md_radial<FP>(b_mul(fa.k, R), g1, g2, f3);
+                    md_radial_r2<FP>(fa, b_norm2(x, y, z), g1, g2, f3);
                     // per-block tables hold the amplitudes (same roundings as in the step)
                     const FP ce = b_mul(s_cos[s0 + j], g1);  // 2 A0 k cos(w t) f1/xi
                     const FP sb = s_sin[s0 + j];             // -2 A0 sin(w t)
