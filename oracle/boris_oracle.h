@@ -14,8 +14,11 @@
  * step by step in the paper's order (L175-186), with no fusion or reordering.
  *
  * Parity pins: see DESIGN.md §4.  All functions below are pinned by
- * `-m "not gpu"` tests in tests/test_oracle_pins.py except where a header
- * comment says "parity unpinned".
+ * `-m "not gpu"` tests in tests/test_oracle_pins.py; oracle_push's sampling of
+ * r- and t-dependent fields at (r^n, t0 + n dt) by tests/test_oracle_driver_pins.py
+ * (exact invariants of plane-wave, m-dipole and grid motion at O(dt^2), each shown to
+ * reject a driver that samples at t_{n+1/2}, at r^{n+1} or ignores t0).  No function
+ * is "parity unpinned".
  */
 #ifndef BORIS_ORACLE_H
 #define BORIS_ORACLE_H
