@@ -268,7 +268,13 @@ Coefs<FP> make_coefs(const boris_ensemble *e, double dt) {
         co.t[i].alpha = (FP)(q * dt / (2.0 * mc));    // eq. 13
         co.t[i].kappa2 = (FP)(kappa * kappa);         // eq. 5
         co.t[i].kappa = (FP)kappa;
+#ifdef BORIS_TEST_PERTURB_CR
+        // test-only tuning build (never the product): a10 off by a relative 1e-4, which
+        // the displacement parity check (tests/parity_util.py Displacement) must reject
+        co.t[i].cr = (FP)(dt / (S * m) * (1.0 + BORIS_TEST_PERTURB_CR));
+#else
         co.t[i].cr = (FP)(dt / (S * m));              // eq. 7
+#endif
         co.t[i].S = (FP)S;
         co.t[i].invS = (FP)(1.0 / S);
         co.t[i].ke = (FP)(1.0 / (S * S * m));         // m c^2 kappa^2

@@ -88,3 +88,48 @@ class OracleRun:
     def kinetic_energy(self):
         return oracle.kinetic_energy(self.mom, self.gamma, self.weight, self.type, self.tm,
                                      self.w.light_velocity)
+
+
+# Unit roundoff of the storage precision: a stored position is fl(r) = r (1 + d), |d| <= u.
+UNIT_ROUNDOFF = {"fp32": 2.0 ** -24, "fp64": 2.0 ** -53}
+
+
+class Displacement:
+    """Reading c15 applied to the displacement dr = r - r0 (eq. 7: the position
+    update is the only place dt/(gamma m) enters r), both sides from the same rounded r0.
+
+    The c15 position metric is floored at the trajectory scale rms|r| (~0.47 lambda in
+    C2/C5), while one C2 step moves a particle by <= c dt = lambda/1e4, so an error in
+    a10 of ~5 % of a step would hide under it.  Two checks on dr instead:
+
+    * per particle: |dr_gpu - dr_ref| - A <= tol (|dr_ref| + S_dr), S_dr the trajectory
+      scale of dr (max over checks of rms|dr_ref|), and A = n_stores u (|r0| + |r_ref| +
+      |dr_ref|) the rounding of the n_stores positions the kernel stored in FP since r0
+      (each fl(r^n) errs by <= u |r^n|; |r^n| <= |r0| + path).  A is what any FP-storage
+      implementation incurs; for fp32 single steps it dominates;
+    * ensemble bias: b = sum_i (dr_gpu - dr_ref).dr_ref / sum_i |dr_ref|^2, the relative
+      scale error of the GPU's displacements.  Storage rounding is unbiased and averages
+      out (noise ~ A/(|dr| sqrt(n))), a systematic error in a10 (e.g. a wrong dt/(S m))
+      does not: |b| <= tol.
+    """
+
+    def __init__(self, r0, precision):
+        self.r0 = np.array(r0, dtype=np.float64, copy=True)
+        self.u = UNIT_ROUNDOFF[precision]
+        self.scale = 0.0
+
+    def __call__(self, r_gpu, r_ref, n_stores, idx=None):
+        r0 = self.r0 if idx is None else self.r0[idx]
+        dg = r_gpu - r0
+        dr = r_ref - r0
+        nrm = np.linalg.norm(dr, axis=1)
+        if nrm.size:
+            self.scale = max(self.scale, float(np.sqrt(np.mean(nrm ** 2))))
+        s = self.scale if self.scale > 0 else 1.0
+        allow = n_stores * self.u * (np.linalg.norm(r0, axis=1) + np.linalg.norm(r_ref, axis=1)
+                                     + nrm)
+        diff = dg - dr
+        err = np.maximum(np.linalg.norm(diff, axis=1) - allow, 0.0) / (nrm + s)
+        den = float(np.sum(dr * dr))
+        bias = float(np.sum(diff * dr)) / den if den > 0 else 0.0
+        return (float(err.max()) if err.size else 0.0), bias

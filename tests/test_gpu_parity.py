@@ -19,7 +19,7 @@ import oracle
 import synth
 import paper_2104_04579_b200 as lb
 from paper_2104_04579_b200.ensemble import AosEnsemble, SoaEnsemble
-from parity_util import TOL, C15, OracleRun, rounded, stack3
+from parity_util import TOL, C15, Displacement, OracleRun, rounded, stack3
 
 pytestmark = pytest.mark.gpu
 
@@ -62,10 +62,12 @@ def gpu_state(ens):
 ORACLE_PUSHER = {0: 0, lb.BORIS_PUSH_PUSHER_VAY: 1, lb.BORIS_PUSH_PUSHER_HIGUERA_CARY: 2}
 
 
-def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False, flags=0):
+def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False, flags=0,
+               check_discrimination=False):
     d, ens, field = build(w, layout, precision, n, host=host)
     ref = OracleRun(w, d, precision, pusher=ORACLE_PUSHER[flags & lb.BORIS_PUSH_PUSHER_MASK])
     metric = C15()
+    disp = Displacement(ref.pos, precision)
     done = 0
     worst = {}
     stream = torch.cuda.current_stream()
@@ -78,6 +80,13 @@ def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False, flag
         r, p, g, st = gpu_state(ens)
         er = metric("r", r, ref.pos)
         ep = metric("p", p, ref.mom)
+        ed, eb = disp(r, ref.pos, s)
+        assert ed <= TOL[precision] and abs(eb) <= TOL[precision], (s, ed, eb)
+        if check_discrimination:
+            # a10 off by 1e-4 (e.g. a mis-rounded dt/(S m)) must fail the displacement check
+            r_bad = disp.r0 + (1 + 1e-4) * (r - disp.r0)
+            ed_bad, eb_bad = disp(r_bad, ref.pos, s)
+            assert max(ed_bad, abs(eb_bad)) > TOL[precision], (s, ed_bad, eb_bad)
         # gamma is derived from p (eq. 5): |d gamma| <= |u| |du| / gamma <= |du|, so the c15
         # bound on p implies |d gamma| <= tol (|u_ref| + S_u), up to gamma's own rounding.
         m = np.array([t[1] for t in w.types])[st["type"].numpy().astype(np.int64)]
@@ -91,12 +100,12 @@ def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False, flag
         g_of_p = np.sqrt(1.0 + np.sum(p * p, 1) / (m * w.light_velocity) ** 2)
         # gamma = g2 * rsqrt(g2) with the <= 2 ulp MUFU rsqrt in fp32 (boris_device.cuh)
         assert np.max(np.abs(g - g_of_p) / g_of_p) <= (1e-6 if precision == "fp32" else 4e-15)
-        worst[s] = (er, ep, eg)
+        worst[s] = (er, ep, eg, ed, eb)
         # order, types, weights untouched (bit-exact)
         assert torch.equal(st["type"], d["type"].to(torch.int16))
         assert torch.equal(st["weight"], d["weight"])
     tol = TOL[precision]
-    for s, (er, ep, eg) in worst.items():
+    for s, (er, ep, eg, ed, eb) in worst.items():
         assert er <= tol and ep <= tol, (s, worst)
     assert lb.boris_ensemble_get_time(ens.handle) == pytest.approx(done * w.dt, rel=1e-15)
     if w.field_kind != "arrays":
@@ -113,7 +122,7 @@ def run_parity(w, layout, precision, n, checks=(1, 2, 10, 100), host=False, flag
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_C2_arrays_parity(layout, precision):
     w = synth.config("C2")
-    worst = run_parity(w, layout, precision, N_SMALL)
+    worst = run_parity(w, layout, precision, N_SMALL, check_discrimination=True)
     print(layout, precision, worst)
 
 
@@ -647,6 +656,8 @@ def _sampled_full_size(name, layout, precision, n_steps, n=None, sample=20_000):
     er = metric("r", r[idx], ref.pos)
     ep = metric("p", p[idx], ref.mom)
     assert er <= TOL[precision] and ep <= TOL[precision], (er, ep)
+    ed, eb = Displacement(stack3(ds, "x", "y", "z"), precision)(r[idx], ref.pos, n_steps)
+    assert ed <= TOL[precision] and abs(eb) <= TOL[precision], (ed, eb)
     if w.field_kind != "arrays":
         lb.boris_field_destroy(field)
     ens.close()
@@ -680,6 +691,8 @@ def test_full_size_C5_bench_configuration():
     metric = C15()
     assert metric("r", r, ref.pos) <= TOL["fp32"]
     assert metric("p", p, ref.mom) <= TOL["fp32"]
+    ed, eb = Displacement(stack3(ds, "x", "y", "z"), "fp32")(r, ref.pos, 1)
+    assert ed <= TOL["fp32"] and abs(eb) <= TOL["fp32"], (ed, eb)
     # KE of the GPU state, summed by the oracle on the host chunk by chunk (Neumaier)
     parts = []
     for c0 in range(0, n, chunk):
@@ -884,6 +897,7 @@ def test_grid_push_parity(precision):
     ref = OracleRun(w, d, precision)
     ref.kind, ref.params, ref.E, ref.B = oracle.FIELD_GRID, params, gE, gB
     metric = C15()
+    disp = Displacement(ref.pos, precision)
     done = 0
     worst = {}
     for s in (1, 10, 100):
@@ -892,10 +906,11 @@ def test_grid_push_parity(precision):
         done = s
         torch.cuda.synchronize()
         r, p, g, st = gpu_state(ens)
-        worst[s] = (metric("r", r, ref.pos), metric("p", p, ref.mom))
+        worst[s] = (metric("r", r, ref.pos), metric("p", p, ref.mom)) + disp(r, ref.pos, s)
     print(precision, worst)
-    for s, (er, ep) in worst.items():
+    for s, (er, ep, ed, eb) in worst.items():
         assert er <= TOL[precision] and ep <= TOL[precision], worst
+        assert ed <= TOL[precision] and abs(eb) <= TOL[precision], worst
     lb.boris_field_destroy(h)
     ens.close()
 
