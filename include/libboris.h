@@ -102,6 +102,25 @@ int32_t boris_abi_version(void);
 const char *boris_status_string(boris_status status);
 const char *boris_last_error(void);
 
+/*
+ * Process-wide options.  The library reads no environment variables; the knobs
+ * tests and tools need are set here.
+ *   BORIS_OPT_FUSED_GENERIC (0 or 1, default 0): 1 turns off the axis-aligned
+ *     specialisation of the register-fused kernels (uniform E on y and B on z;
+ *     plane wave along x polarised along y), so those pushes run the generic
+ *     kernel.  Results are bitwise identical (the specialisation only skips
+ *     products with exact zeros); for tests that cover both kernels.
+ *   BORIS_OPT_HOST_CHUNK (particles, default 4194304): chunk size of the
+ *     host-resident (BORIS_MEMORY_HOST) push pipeline; must be >= 1024, used
+ *     rounded down to a multiple of 8.
+ * A new value applies to pushes issued after the call.  Errors: INVALID_ARG
+ * (unknown option, value out of range, NULL out-pointer).
+ */
+#define BORIS_OPT_FUSED_GENERIC 1
+#define BORIS_OPT_HOST_CHUNK 2
+boris_status boris_set_option(int32_t option, int64_t value);
+boris_status boris_get_option(int32_t option, int64_t *value);
+
 /* ------------------------------------------------------------------------ */
 /* Ensembles (paper §3 "Data Structures", L193-254)                           */
 /* ------------------------------------------------------------------------ */
@@ -307,7 +326,8 @@ boris_status boris_push_deposit(boris_ensemble *ens, const boris_field *grid, do
  * position r_i at time t and write it into the per-particle field `out` (arrays
  * created with boris_field_create_arrays_* for `ens`; layout, precision, n,
  * device and residency must match, else MISMATCH).  The values are those the
- * fused push would use at (r_i, t).  Device ensembles only.  Asynchronous.
+ * fused push would use at (r_i, t) (the same arithmetic).  Device ensembles
+ * only.  Asynchronous.
  */
 boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensemble *ens,
                                   double t, const boris_field *out, void *stream);

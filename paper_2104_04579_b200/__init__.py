@@ -43,12 +43,15 @@ BORIS_PUSH_PUSHER_BORIS = 0x00
 BORIS_PUSH_PUSHER_VAY = 0x10
 BORIS_PUSH_PUSHER_HIGUERA_CARY = 0x20
 BORIS_PUSH_PUSHER_MASK = 0x30
+BORIS_OPT_FUSED_GENERIC = 1
+BORIS_OPT_HOST_CHUNK = 2
 BORIS_AOS_RECORD_BYTES = {BORIS_FP32: 36, BORIS_FP64: 72}
 BORIS_AOS_FIELD_BYTES = {BORIS_FP32: 24, BORIS_FP64: 48}
 
 # Every symbol include/libboris.h declares (checked by tests/test_abi_cpu.py).
 EXPORTED = (
     "boris_abi_version", "boris_status_string", "boris_last_error",
+    "boris_set_option", "boris_get_option",
     "boris_ensemble_create", "boris_ensemble_wrap_soa", "boris_ensemble_wrap_aos",
     "boris_ensemble_destroy", "boris_ensemble_upload", "boris_ensemble_download",
     "boris_ensemble_validate_types", "boris_ensemble_get_info", "boris_ensemble_get_time",
@@ -84,6 +87,8 @@ _SIGNATURES = {
     "boris_abi_version": ([], _i32),
     "boris_status_string": ([_i32], ctypes.c_char_p),
     "boris_last_error": ([], ctypes.c_char_p),
+    "boris_set_option": ([_i32, _i64], _i32),
+    "boris_get_option": ([_i32, ctypes.POINTER(_i64)], _i32),
     "boris_ensemble_create": ([_i32, _i32, _i32, _i64, _tp, _i32, _d, _hp], _i32),
     "boris_ensemble_wrap_soa": ([_i32, _i32, _i32, _i64] + [_vp] * 9 + [_tp, _i32, _d, _hp], _i32),
     "boris_ensemble_wrap_aos": ([_i32, _i32, _i32, _i64, _vp, _tp, _i32, _d, _hp], _i32),
@@ -186,6 +191,16 @@ def boris_status_string(status: int) -> str:
 
 def boris_last_error() -> str:
     return load_library().boris_last_error().decode()
+
+
+def boris_set_option(option: int, value: int):
+    _check(load_library().boris_set_option(option, value), "boris_set_option")
+
+
+def boris_get_option(option: int) -> int:
+    v = _i64()
+    _check(load_library().boris_get_option(option, ctypes.byref(v)), "boris_get_option")
+    return int(v.value)
 
 
 # ---------------------------------------------------------------------------

@@ -10,8 +10,13 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <atomic>
 
 #include "boris_internal.h"
+
+// Process-wide options (boris_set_option); the library reads no environment.
+static std::atomic<int64_t> g_opt_fused_generic{0};
+static std::atomic<int64_t> g_opt_host_chunk{(int64_t)4 << 20};
 
 using namespace boris;
 
@@ -332,9 +337,8 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
         a.grid = make_grid_args<FP>(f);
     }
     // exact zeros off the y (E) and z (B) axes -> the YZ fused specialisation;
-    // BORIS_FUSED_GENERIC=1 (read per push) forces the generic kernel (tests)
-    const char *gen = getenv("BORIS_FUSED_GENERIC");
-    const bool allow = !(gen && gen[0] == '1');
+    // BORIS_OPT_FUSED_GENERIC = 1 forces the generic kernel (tests)
+    const bool allow = g_opt_fused_generic.load(std::memory_order_relaxed) == 0;
     if (allow && f->kind == FK_UNIFORM)
         a.yz = a.E[0] == 0 && a.E[2] == 0 && a.B[0] == 0 && a.B[1] == 0;
     else if (allow && f->kind == FK_PLANE_WAVE)
@@ -403,12 +407,7 @@ boris_status check_push_args(const boris_ensemble *e, const boris_field *f, doub
 // ---------------------------------------------------------------------------
 // Host-resident ensembles: chunked H2D -> push -> D2H pipeline (double buffer).
 // ---------------------------------------------------------------------------
-int64_t host_chunk_particles() {
-    const char *s = getenv("BORIS_HOST_CHUNK");
-    int64_t v = s ? atoll(s) : (int64_t)(4 << 20);
-    if (v < 1024) v = 1024;
-    return v / 8 * 8;
-}
+int64_t host_chunk_particles() { return g_opt_host_chunk.load(std::memory_order_relaxed) / 8 * 8; }
 
 static boris_status build_pipeline(const boris_ensemble *e, bool with_fields, HostPipeline *p);
 
@@ -603,6 +602,33 @@ const char *boris_status_string(boris_status s) {
 }
 
 const char *boris_last_error(void) { return g_last_error.c_str(); }
+
+boris_status boris_set_option(int32_t option, int64_t value) {
+    switch (option) {
+    case BORIS_OPT_FUSED_GENERIC:
+        if (value != 0 && value != 1)
+            return fail(BORIS_E_INVALID_ARG, "BORIS_OPT_FUSED_GENERIC must be 0 or 1");
+        g_opt_fused_generic.store(value);
+        return BORIS_OK;
+    case BORIS_OPT_HOST_CHUNK:
+        if (value < 1024 || value > BORIS_MAX_PARTICLES)
+            return fail(BORIS_E_INVALID_ARG, "BORIS_OPT_HOST_CHUNK = %lld outside [1024, 2^40]",
+                        (long long)value);
+        g_opt_host_chunk.store(value);
+        return BORIS_OK;
+    default:
+        return fail(BORIS_E_INVALID_ARG, "unknown option %d", option);
+    }
+}
+
+boris_status boris_get_option(int32_t option, int64_t *value) {
+    if (!value) return fail(BORIS_E_INVALID_ARG, "value is NULL");
+    switch (option) {
+    case BORIS_OPT_FUSED_GENERIC: *value = g_opt_fused_generic.load(); return BORIS_OK;
+    case BORIS_OPT_HOST_CHUNK: *value = g_opt_host_chunk.load(); return BORIS_OK;
+    default: return fail(BORIS_E_INVALID_ARG, "unknown option %d", option);
+    }
+}
 
 boris_status boris_ensemble_create(int32_t device, boris_layout layout, boris_precision precision,
                                    int64_t n, const boris_particle_type *types, int32_t n_types,

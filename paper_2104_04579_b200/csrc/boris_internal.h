@@ -107,15 +107,6 @@ cudaError_t launch_stream_soa_grid(const EnsView &e, const GridArgs<FP> &g, cons
                                    bool multi, DiagOut *diag, int device, cudaStream_t st);
 
 template <typename FP>
-cudaError_t launch_stream_soa_grid_tma(const EnsView &e, const GridArgs<FP> &g,
-                                       const Coefs<FP> &co, bool multi, DiagOut *diag,
-                                       int device, cudaStream_t st);
-
-template <typename FP>
-cudaError_t launch_stream_soa_tma(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
-                                  bool multi, DiagOut *diag, int device, cudaStream_t st);
-
-template <typename FP>
 cudaError_t launch_stream_aos(const EnsView &e, const void *field_records, const Coefs<FP> &co,
                               bool multi, DiagOut *diag, int device, cudaStream_t st);
 

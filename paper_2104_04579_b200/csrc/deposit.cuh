@@ -139,4 +139,182 @@ struct DepositRun {
     }
 };
 
+// ---------------------------------------------------------------------------
+// Warp-run deposition (sorted input): the lanes of a warp hold 32 CONSECUTIVE
+// particles per round (coalesced 4/8 B loads), so after sorting by cell a round
+// almost always lies in one cell.  Every lane accumulates its particles of the
+// warp's open cell in 8 x 3 registers; when a round leaves the open cell the 24
+// sums are reduced across the warp through shared memory (transposed: lane t < 24
+// adds row t = component t of all 32 lanes) and written with ONE 24-lane atomic
+// instruction.  Per particle: one all-vote, the CIC weights and 24 FMA; the
+// reduction is paid once per cell, not per particle or per lane.  Lanes of a
+// round whose cell is neither the open one nor the round's newest cell (unsorted
+// input) deposit their own particle with 24 scalar atomics.
+// ---------------------------------------------------------------------------
+template <typename FP>
+struct WarpRunSmem {
+    static constexpr int RS = sizeof(FP) == 4 ? 36 : 34;  // row stride (FP): conflict-free
+    FP red[24 * RS];
+};
+
+template <typename FP>
+struct WarpRun {
+    FP acc[8][3];
+    FP oc[3];   // open cell's unwrapped floor((r - org)/h) (warp-uniform)
+    bool open;  // warp-uniform
+
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+        oc[0] = oc[1] = oc[2] = FP(0);
+        open = false;
+    }
+
+    // One particle's CIC data: unwrapped cell l, node weights sw (q = (c*2+b)*2+a),
+    // and q w v / volume.
+    struct Part {
+        FP l[3];
+        FP sw[8];
+        FP qv[3];
+    };
+
+    static __device__ __forceinline__ void prepare(const GridArgs<FP> &g, const DepCoef<FP> &t,
+                                                   FP half_dt, FP x, FP y, FP z, FP px, FP py,
+                                                   FP pz, FP w, Part &p) {
+        const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
+        const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
+        const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
+        FP f[3];
+        p.l[0] = DepositRun<FP>::axis_floor(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], f[0]);
+        p.l[1] = DepositRun<FP>::axis_floor(b_fma(-half_dt, vy, y), g.org[1], g.inv_h[1], f[1]);
+        p.l[2] = DepositRun<FP>::axis_floor(b_fma(-half_dt, vz, z), g.org[2], g.inv_h[2], f[2]);
+        const FP qw = b_mul(t.q_vol, w);
+        p.qv[0] = b_mul(qw, vx);
+        p.qv[1] = b_mul(qw, vy);
+        p.qv[2] = b_mul(qw, vz);
+        const FP wx[2] = {b_add(FP(1), -f[0]), f[0]};
+        const FP wy[2] = {b_add(FP(1), -f[1]), f[1]};
+        const FP wz[2] = {b_add(FP(1), -f[2]), f[2]};
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const FP wyz = b_mul(wy[b], wz[c]);
+#pragma unroll
+                for (int a = 0; a < 2; ++a) p.sw[(c * 2 + b) * 2 + a] = b_mul(wx[a], wyz);
+            }
+    }
+
+    __device__ __forceinline__ void add(const Part &p) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) acc[q][d] = b_fma(p.sw[q], p.qv[d], acc[q][d]);
+    }
+
+    // Nodes of the cell with unwrapped floor l (periodic wrap): corner q = (c*2+b)*2+a
+    // is row(b, c) + i[a].
+    struct Nodes {
+        uint32_t row[4];
+        int i[2];
+        __device__ __forceinline__ uint32_t operator()(int q) const {
+            return row[q >> 1] + (uint32_t)i[q & 1];
+        }
+    };
+    static __device__ __forceinline__ Nodes nodes(const GridArgs<FP> &g, const FP (&l)[3]) {
+        Nodes nd;
+        int j[2], k[2];
+        DepositRun<FP>::axis_wrap(l[0], g.nf[0], g.inv_nf[0], g.n[0], nd.i[0], nd.i[1]);
+        DepositRun<FP>::axis_wrap(l[1], g.nf[1], g.inv_nf[1], g.n[1], j[0], j[1]);
+        DepositRun<FP>::axis_wrap(l[2], g.nf[2], g.inv_nf[2], g.n[2], k[0], k[1]);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+                nd.row[c * 2 + b] = ((uint32_t)k[c] * (uint32_t)g.n[1] + (uint32_t)j[b]) *
+                                    (uint32_t)g.n[0];
+        return nd;
+    }
+
+    // Warp-wide: reduce the 24 sums over the lanes and add them to J at the open
+    // cell's nodes (one atomic instruction, lanes 0..23); zero the sums.
+    __device__ __forceinline__ void flush(const GridArgs<FP> &g, FP *Jx, FP *Jy, FP *Jz,
+                                          WarpRunSmem<FP> &sm, int lane) {
+        constexpr int RS = WarpRunSmem<FP>::RS;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                sm.red[(q * 3 + d) * RS + lane] = acc[q][d];
+                acc[q][d] = FP(0);
+            }
+        __syncwarp();
+        if (lane < 24) {
+            const FP *row = sm.red + lane * RS;
+            FP s;
+            if constexpr (sizeof(FP) == 4) {
+                float4 a = reinterpret_cast<const float4 *>(row)[0];
+#pragma unroll
+                for (int k = 1; k < 8; ++k) {
+                    const float4 v = reinterpret_cast<const float4 *>(row)[k];
+                    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                }
+                s = (a.x + a.y) + (a.z + a.w);
+            } else {
+                double2 a = reinterpret_cast<const double2 *>(row)[0];
+#pragma unroll
+                for (int k = 1; k < 16; ++k) {
+                    const double2 v = reinterpret_cast<const double2 *>(row)[k];
+                    a.x += v.x;
+                    a.y += v.y;
+                }
+                s = a.x + a.y;
+            }
+            const int q = lane / 3, d = lane - 3 * (lane / 3);
+            FP *J = d == 0 ? Jx : (d == 1 ? Jy : Jz);
+            if (s != FP(0)) atomicAdd(J + nodes(g, oc)(q), s);
+        }
+        __syncwarp();
+    }
+
+    // One particle straight to J (a lane outside the round's open cells).
+    static __device__ __forceinline__ void deposit_single(const GridArgs<FP> &g, const Part &p,
+                                                          FP *Jx, FP *Jy, FP *Jz) {
+        const Nodes nds = nodes(g, p.l);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t nd = nds(q);
+            atomicAdd(Jx + nd, b_mul(p.sw[q], p.qv[0]));
+            atomicAdd(Jy + nd, b_mul(p.sw[q], p.qv[1]));
+            atomicAdd(Jz + nd, b_mul(p.sw[q], p.qv[2]));
+        }
+    }
+
+    // One round (all 32 lanes; an invalid lane passes qv = 0 and valid = false).
+    __device__ __forceinline__ void round(const GridArgs<FP> &g, const Part &p, bool valid,
+                                          FP *Jx, FP *Jy, FP *Jz, WarpRunSmem<FP> &sm,
+                                          int lane) {
+        const unsigned full = 0xffffffffu;
+        const bool in_open =
+            !valid || (open && p.l[0] == oc[0] && p.l[1] == oc[1] && p.l[2] == oc[2]);
+        if (__all_sync(full, in_open)) {
+            add(p);  // invalid lanes add exact zeros
+            return;
+        }
+        if (in_open && valid) add(p);
+        if (open) flush(g, Jx, Jy, Jz, sm, lane);
+        // the newest cell of the round (highest lane outside the open cell) opens
+        const unsigned rest = __ballot_sync(full, !in_open);
+        const int leader = 31 - __clz(rest);
+        oc[0] = __shfl_sync(full, p.l[0], leader);
+        oc[1] = __shfl_sync(full, p.l[1], leader);
+        oc[2] = __shfl_sync(full, p.l[2], leader);
+        open = true;
+        if (!in_open) {
+            if (p.l[0] == oc[0] && p.l[1] == oc[1] && p.l[2] == oc[2]) add(p);
+            else deposit_single(g, p, Jx, Jy, Jz);
+        }
+    }
+};
+
 }  // namespace boris

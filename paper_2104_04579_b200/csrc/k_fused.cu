@@ -31,14 +31,6 @@ __device__ __forceinline__ float cos_reduced(double phi, float) {
 }
 __device__ __forceinline__ double cos_reduced(double phi, double) { return cos(phi); }
 
-__device__ __forceinline__ void sincos_fp(double a, double *s, double *c) { sincos(a, s, c); }
-__device__ __forceinline__ void sincos_fp(double a, float *s, float *c) {
-    const double q = rint(a * kInvTwoPi);
-    double r = fma(-q, kTwoPiHi, a);
-    r = fma(-q, kTwoPiLo, r);
-    sincosf((float)r, s, c);
-}
-
 // phi mod 2 pi in [-pi, pi] (Cody-Waite, exact for |phi| < 2^40).
 __device__ __forceinline__ double reduce_2pi(double phi) {
     const double q = rint(phi * kInvTwoPi);
@@ -214,21 +206,23 @@ __device__ __forceinline__ void analytic_field(const AnalyticArgs<FP> &fa, doubl
     } else if constexpr (FIELD == FK_GRID) {
         grid_gather<FP>(fa.grid, (FP)rx, (FP)ry, (FP)rz, Ex, Ey, Ez, Bx, By, Bz);
     } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
+        // the fused step's arithmetic (k_fused below): radial functions from r^2, the
+        // time amplitudes rounded as its per-block tables, the same product order
         const FP x = (FP)rx, y = (FP)ry, z = (FP)rz;
-        const FP R = sqrt(x * x + y * y + z * z);
         FP g1, g2, f3;
-        md_radial<FP>(fa.k * R, g1, g2, f3);
-        FP swt, cwt;
-        sincos_fp(fa.w0t0 + (double)n * fa.w0dt, &swt, &cwt);
-        const FP ce = FP(2) * fa.A0 * cwt * fa.k * g1;  // 2 A0 cos(w t) f1/R
-        const FP sb = FP(-2) * fa.A0 * swt;              // -2 A0 sin(w t)
-        const FP k2g2 = fa.k2 * g2;                      // f2/R^2
-        Ex = -ce * y;
-        Ey = ce * x;
+        md_radial_r2<FP>(fa, b_norm2(x, y, z), g1, g2, f3);
+        double sn, cs;
+        sincos(fa.w0t0 + (double)n * fa.w0dt, &sn, &cs);  // t_n = t0 + n dt (c5)
+        const FP ce = b_mul(b_mul(fa.A0k2, (FP)cs), g1);    // 2 A0 k cos(w t) f1/xi
+        const FP sb = b_mul(fa.mA02, (FP)sn);               // -2 A0 sin(w t)
+        const FP k2g2 = b_mul(fa.k2, g2);                   // f2/R^2
+        Ex = -b_mul(ce, y);
+        Ey = b_mul(ce, x);
         Ez = FP(0);
-        Bx = sb * k2g2 * x * z;
-        By = sb * k2g2 * y * z;
-        Bz = sb * (k2g2 * z * z + f3);
+        const FP sk = b_mul(sb, k2g2);
+        Bx = b_mul(b_mul(sk, x), z);
+        By = b_mul(b_mul(sk, y), z);
+        Bz = b_mul(sb, b_fma(k2g2, b_mul(z, z), f3));
     }
 }
 

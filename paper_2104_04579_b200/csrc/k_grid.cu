@@ -258,92 +258,134 @@ __global__ void k_gather_bytes(const unsigned char *in, unsigned char *out, cons
     }
 }
 
-// All SoA arrays at once: blk[a*fb + i] = arr_a[perm[i]] (perm read once per i).
-// Four particles per thread: one 128-bit perm load, four independent gathers per
-// array (more loads in flight), 128-bit stores into the 256 B-aligned slices.
+// SoA permutation by particle records.  A permutation from random order gathers
+// every array at random indices; a 4 B gather costs a whole DRAM access, so eight
+// separate array gathers moved ~740 B per particle (ncu, 10^7, random order).
+// Instead: (1) k_pack_soa writes each particle's present arrays as one record of
+// RS FP slots (x y z px py pz [w] [g] [type]) with coalesced reads; (2)
+// k_unpack_soa reads record perm[i] (RS adjacent slots: 1-2 sectors) and writes
+// slot a to array a at i, coalesced, straight into the ensemble's own arrays (the
+// records are the only copy, so no copy-back pass).  From sorted order the record
+// reads are sequential too, so the traffic is the same as gather + copy-back.
+struct PermPlan {
+    void *arr[8];  // present FP arrays in record-slot order
+    int nf;        // number of FP slots before the type slot
+    int16_t *type; // null: no type slot
+    int rs;        // record stride in FP slots
+};
+
+static PermPlan perm_plan(const SoaPtrs &s) {
+    PermPlan p{};
+    void *all[8] = {s.x, s.y, s.z, s.px, s.py, s.pz, s.w, s.g};
+    for (int a = 0; a < 8; ++a)
+        if (all[a]) p.arr[p.nf++] = all[a];
+    p.type = s.type;
+    p.rs = p.nf + (s.type ? 1 : 0);
+    return p;
+}
+
+// Records whose size is a multiple of 16 B (x y z px py pz w g without a type slot)
+// are written straight from registers with 16 B vector stores.  Otherwise the
+// records of a 256-particle tile are assembled in shared memory (thread t writes
+// slots t*RS + a; RS = 9 is odd, so fp32 writes are conflict-free) and leave as
+// contiguous 16 B vector stores: every written sector is written whole either way
+// (scalar stores at a 36 B lane stride took 3x the time of the traffic).
+constexpr int kPackTile = 256;
+
 template <typename FP>
-__global__ void __launch_bounds__(256)
-    k_permute_soa(SoaPtrs s, const uint32_t *perm, int64_t n, unsigned char *blk, size_t fb) {
-    const FP *src[8] = {(const FP *)s.x, (const FP *)s.y, (const FP *)s.z, (const FP *)s.px,
-                        (const FP *)s.py, (const FP *)s.pz, (const FP *)s.w, (const FP *)s.g};
-    const int64_t ng = n / 4;
+__global__ void __launch_bounds__(kPackTile)
+    k_pack_soa_vec(const __grid_constant__ PermPlan p, int64_t n, FP *rec) {
+    constexpr int V = 16 / sizeof(FP);  // FP per 16 B vector
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < ng; q += stride) {
-        const uint4 j4 = __ldg(reinterpret_cast<const uint4 *>(perm) + q);
-        const uint32_t j[4] = {j4.x, j4.y, j4.z, j4.w};
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            if (!src[a]) continue;
-            FP v[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v[k] = src[a][j[k]];
-            FP *out = (FP *)(blk + a * fb) + 4 * q;
-            if constexpr (sizeof(FP) == 4) {
-                *reinterpret_cast<float4 *>(out) = make_float4(v[0], v[1], v[2], v[3]);
-            } else {
-                reinterpret_cast<double2 *>(out)[0] = make_double2(v[0], v[1]);
-                reinterpret_cast<double2 *>(out)[1] = make_double2(v[2], v[3]);
-            }
-        }
-        if (s.type) {
-            int16_t t[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) t[k] = s.type[j[k]];
-            const uint2 tv = make_uint2((uint32_t)(uint16_t)t[0] | ((uint32_t)(uint16_t)t[1] << 16),
-                                        (uint32_t)(uint16_t)t[2] | ((uint32_t)(uint16_t)t[3] << 16));
-            *reinterpret_cast<uint2 *>((int16_t *)(blk + 8 * fb) + 4 * q) = tv;
-        }
-    }
-    // ragged tail (n mod 4)
-    const int64_t i = 4 * ng + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        const int64_t jj = perm[i];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        FP v[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a)
-            if (src[a]) ((FP *)(blk + a * fb))[i] = src[a][jj];
-        if (s.type) ((int16_t *)(blk + 8 * fb))[i] = s.type[jj];
+            if (a < p.nf) v[a] = ((const FP *)p.arr[a])[i];
+        uint4 *r = reinterpret_cast<uint4 *>(rec + i * p.rs);
+#pragma unroll
+        for (int k = 0; k < 8 / V; ++k)
+            if (k * V < p.nf) {
+                uint4 u;
+                memcpy(&u, v + k * V, 16);
+                r[k] = u;
+            }
     }
 }
 
-// Copy the permuted slices back into the ensemble's arrays: 128-bit accesses when
-// every destination is 16 B-aligned (owned ensembles, most torch tensors), all
-// slices of a 4-particle group loaded before any store (ILP); scalar otherwise.
+template <typename FP>
+__global__ void __launch_bounds__(kPackTile)
+    k_pack_soa(const __grid_constant__ PermPlan p, int64_t n, FP *rec) {
+    using W = typename std::conditional<sizeof(FP) == 4, uint32_t, unsigned long long>::type;
+    extern __shared__ __align__(16) unsigned char pack_smem[];
+    FP *tile = reinterpret_cast<FP *>(pack_smem);
+    const int64_t ntiles = (n + kPackTile - 1) / kPackTile;
+    const int t = threadIdx.x;
+    for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
+        const int64_t i0 = tb * kPackTile;
+        const int cnt = (int)(n - i0 < kPackTile ? n - i0 : kPackTile);
+        if (t < cnt) {
+            const int64_t i = i0 + t;
+            FP v[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (a < p.nf) v[a] = ((const FP *)p.arr[a])[i];
+            FP *r = tile + t * p.rs;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (a < p.nf) r[a] = v[a];
+            if (p.type) reinterpret_cast<W *>(r)[p.nf] = (W)(uint16_t)p.type[i];
+        }
+        __syncthreads();
+        // cnt * rs FP values, contiguous at rec + i0 * rs (16 B aligned: i0 * rs * sizeof(FP)
+        // is a multiple of 256 * 4 B)
+        const int64_t words = (int64_t)cnt * p.rs;
+        const int nvec = (int)(words * sizeof(FP) / 16);
+        uint4 *dst = reinterpret_cast<uint4 *>(rec + i0 * p.rs);
+        const uint4 *src = reinterpret_cast<const uint4 *>(tile);
+        for (int k = t; k < nvec; k += kPackTile) dst[k] = src[k];
+        for (int64_t k = (int64_t)nvec * 16 / sizeof(FP) + t; k < words; k += kPackTile)
+            rec[i0 * p.rs + k] = tile[k];
+        __syncthreads();
+    }
+}
+
+// Four particles per thread (i = base + k*256 + tid): 4 x RS independent record
+// loads in flight, every store warp-coalesced.
 template <typename FP>
 __global__ void __launch_bounds__(256)
-    k_copy_back_soa(SoaPtrs s, int64_t n, const unsigned char *blk, size_t fb, bool vec) {
-    FP *dst[8] = {(FP *)s.x, (FP *)s.y, (FP *)s.z, (FP *)s.px,
-                  (FP *)s.py, (FP *)s.pz, (FP *)s.w, (FP *)s.g};
-    using V = typename std::conditional<sizeof(FP) == 4, float4, double2>::type;
-    constexpr int W = 16 / sizeof(FP);  // particles per 128-bit vector
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t done = 0;
-    if (vec) {
-        const int64_t ng = n / 8;  // groups of 8 particles: W-multiples for both FP
-        for (int64_t q = t0; q < ng; q += stride) {
-            V v[8][8 / W];
+    k_unpack_soa(const __grid_constant__ PermPlan p, const uint32_t *perm, int64_t n,
+                 const FP *rec) {
+    using W = typename std::conditional<sizeof(FP) == 4, uint32_t, unsigned long long>::type;
+    constexpr int U = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U; base < n; base += stride) {
+        int64_t j[U];
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int h = 0; h < 8 / W; ++h)
-                    if (dst[a])
-                        v[a][h] = reinterpret_cast<const V *>(blk + a * fb)[q * (8 / W) + h];
-            uint4 tv;
-            if (s.type) tv = reinterpret_cast<const uint4 *>(blk + 8 * fb)[q];
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int h = 0; h < 8 / W; ++h)
-                    if (dst[a]) reinterpret_cast<V *>(dst[a])[q * (8 / W) + h] = v[a][h];
-            if (s.type) reinterpret_cast<uint4 *>(s.type)[q] = tv;
+        for (int k = 0; k < U; ++k) {
+            const int64_t i = base + k * blockDim.x + threadIdx.x;
+            j[k] = i < n ? (int64_t)__ldg(perm + i) : -1;
         }
-        done = 8 * ng;
-    }
-    for (int64_t i = done + t0; i < n; i += stride) {
+        FP v[U][8];
+        W t[U];
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-            if (dst[a]) dst[a][i] = ((const FP *)(blk + a * fb))[i];
-        if (s.type) s.type[i] = ((const int16_t *)(blk + 8 * fb))[i];
+        for (int k = 0; k < U; ++k) {
+            if (j[k] < 0) continue;
+            const FP *r = rec + j[k] * p.rs;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (a < p.nf) v[k][a] = __ldg(r + a);
+            if (p.type) t[k] = __ldg(reinterpret_cast<const W *>(r) + p.nf);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            if (j[k] < 0) continue;
+            const int64_t i = base + k * blockDim.x + threadIdx.x;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (a < p.nf) ((FP *)p.arr[a])[i] = v[k][a];
+            if (p.type) p.type[i] = (int16_t)(uint16_t)t[k];
+        }
     }
 }
 
@@ -405,23 +447,22 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     // v0 = sorted original indices: apply to every particle array
     if (err == cudaSuccess) {
         if (e.layout == BORIS_LAYOUT_SOA) {
-            // one gather kernel for all arrays into a scratch block, then copy back
-            unsigned char *blk = nullptr;
-            const size_t fb = ((size_t)n * sizeof(FP) + 255) / 256 * 256;
-            err = scratch_alloc((void **)&blk, 8 * fb + (size_t)n * 2 + 256, st);
+            // pack records, then gather them through the permutation into the arrays
+            const PermPlan plan = perm_plan(e.soa);
+            FP *rec = nullptr;
+            err = scratch_alloc((void **)&rec, (size_t)n * plan.rs * sizeof(FP), st);
             if (err == cudaSuccess) {
-                k_permute_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(e.soa, v0, n, blk, fb);
+                const size_t smem = (size_t)kPackTile * plan.rs * sizeof(FP);
+                if (!plan.type && plan.rs * sizeof(FP) % 16 == 0)
+                    k_pack_soa_vec<FP><<<grid1d(n), kPackTile, 0, st>>>(plan, n, rec);
+                else
+                    k_pack_soa<FP><<<grid1d(n), kPackTile, smem, st>>>(plan, n, rec);
                 err = cudaGetLastError();
-                if (err == cudaSuccess) {  // one copy-back launch for all arrays
-                    auto al16 = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
-                    const bool vec = al16(e.soa.x) && al16(e.soa.y) && al16(e.soa.z) &&
-                                     al16(e.soa.px) && al16(e.soa.py) && al16(e.soa.pz) &&
-                                     al16(e.soa.w) && al16(e.soa.g) && al16(e.soa.type);
-                    k_copy_back_soa<FP><<<grid1d((n + 7) / 8), 256, 0, st>>>(e.soa, n, blk, fb,
-                                                                              vec);
+                if (err == cudaSuccess) {
+                    k_unpack_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(plan, v0, n, rec);
                     err = cudaGetLastError();
                 }
-                scratch_free(blk, st);
+                scratch_free(rec, st);
             }
         } else {
             err = permute_array<RB>(e.aos, tmp, v0, n, st);
@@ -549,24 +590,9 @@ struct DepRuns {
     static constexpr int SK = TILE + TILE / K;
 };
 
-static bool deposit_runs_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *s = getenv("BORIS_DEPOSIT_KERNEL");
-        v = (s && s[0] == 'w') ? 0 : 1;  // "warp" selects the warp-scan kernel
-    }
-    return v == 1;
-}
-
-// DIRECT (fp32, 16 B aligned arrays): no shared-memory staging; each lane loads
-// its K = 8 consecutive particles with two 128-bit loads per array (a warp's
-// loads cover the tile contiguously) and keeps them in registers.
-// BORIS_DEPOSIT_STAGING=smem keeps the shared-memory staged kernel for fp32 too.
-static bool deposit_direct_enabled() {
-    const char *s = getenv("BORIS_DEPOSIT_STAGING");
-    return !(s && s[0] == 's');
-}
-
+// fp32 with 16 B-aligned arrays: DIRECT (no shared-memory staging; each lane
+// loads its K = 8 consecutive particles with two 128-bit loads per array, a
+// warp's loads cover the tile contiguously).  fp64 or unaligned: staged tiles.
 #ifndef BORIS_DEP_PREFETCH
 #define BORIS_DEP_PREFETCH 0
 #endif
@@ -687,6 +713,76 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-run deposition (SoA, any alignment; deposit.cuh WarpRun): each warp owns a
+// contiguous chunk of particles and walks it in rounds of 32 consecutive
+// particles (lane l takes particle base + l: 4/8 B loads, warp-coalesced), PD
+// rounds of loads in flight ahead of the arithmetic (register ring).  Sorted by
+// cell, a round almost always lies in the warp's open cell: 24 FMA per particle,
+// one warp reduction + one 24-lane atomic instruction per cell.
+// ---------------------------------------------------------------------------
+#ifndef BORIS_DW_PD
+#define BORIS_DW_PD 3
+#endif
+#ifndef BORIS_DW_MINB
+#define BORIS_DW_MINB 2
+#endif
+template <typename FP>
+struct DepWarp {
+    static constexpr int WARPS = sizeof(FP) == 4 ? 8 : 4;  // warps per block (static smem)
+    static constexpr int PD = BORIS_DW_PD;                  // rounds of loads in flight
+    static constexpr int MINB = sizeof(FP) == 4 ? BORIS_DW_MINB : 2;  // blocks per SM
+};
+
+template <typename FP, bool MULTI>
+__global__ void __launch_bounds__(DepWarp<FP>::WARPS * 32, DepWarp<FP>::MINB)
+    k_deposit_warp(EnsView e, const __grid_constant__ GridArgs<FP> g,
+                   const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz,
+                   int64_t chunk) {
+    using D = DepWarp<FP>;
+    constexpr int PD = D::PD;
+    __shared__ WarpRunSmem<FP> sm[D::WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t begin = ((int64_t)blockIdx.x * D::WARPS + warp) * chunk;
+    if (begin >= e.n) return;  // warp-uniform; no block barrier follows
+    const int64_t end = begin + chunk < e.n ? begin + chunk : e.n;
+    FP buf[PD][7];
+    int ty[PD];
+    // array bases stay in the parameter bank (no pointer registers)
+    auto load = [&](int k, int64_t i) {
+        const bool ok = i < end;
+        buf[k][0] = ok ? __ldg((const FP *)e.soa.x + i) : FP(0);
+        buf[k][1] = ok ? __ldg((const FP *)e.soa.y + i) : FP(0);
+        buf[k][2] = ok ? __ldg((const FP *)e.soa.z + i) : FP(0);
+        buf[k][3] = ok ? __ldg((const FP *)e.soa.px + i) : FP(0);
+        buf[k][4] = ok ? __ldg((const FP *)e.soa.py + i) : FP(0);
+        buf[k][5] = ok ? __ldg((const FP *)e.soa.pz + i) : FP(0);
+        buf[k][6] = ok ? (e.soa.w ? __ldg((const FP *)e.soa.w + i) : FP(1)) : FP(0);  // w = 0: no current
+        ty[k] = (MULTI && ok) ? (int)__ldg(e.soa.type + i) : 0;
+    };
+#pragma unroll
+    for (int k = 0; k < PD; ++k) load(k, begin + 32 * k + lane);
+    WarpRun<FP> run;
+    run.reset();
+    for (int64_t base = begin; base < end; base += 32 * PD) {
+#pragma unroll
+        for (int k = 0; k < PD; ++k) {
+            if (base + 32 * k >= end) break;  // warp-uniform
+            const int64_t i = base + 32 * k + lane;
+            FP v[7];
+#pragma unroll
+            for (int a = 0; a < 7; ++a) v[a] = buf[k][a];
+            const int t = ty[k];
+            load(k, i + 32 * PD);
+            typename WarpRun<FP>::Part part;
+            WarpRun<FP>::prepare(g, dc.t[MULTI ? t : 0], dc.half_dt, v[0], v[1], v[2], v[3],
+                                 v[4], v[5], v[6], part);
+            run.round(g, part, i < end, Jx, Jy, Jz, sm[warp], lane);
+        }
+    }
+    if (run.open) run.flush(g, Jx, Jy, Jz, sm[warp], lane);
+}
+
 template <typename FP>
 __global__ void k_zero3(FP *a, FP *b, FP *c, int64_t n) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -714,27 +810,38 @@ cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoe
     const int64_t ncell = (int64_t)g.n[0] * g.n[1] * g.n[2];
     cudaError_t err = launch_zero3<FP>(Jx, Jy, Jz, ncell, st);
     if (err != cudaSuccess || e.n == 0) return err;
-    if (e.layout == BORIS_LAYOUT_SOA && deposit_runs_enabled()) {
-        using R = DepRuns<FP>;
-        const int64_t tiles = (e.n + R::TILE - 1) / R::TILE;
+    // fp32 with 16 B-aligned arrays: lane runs (k_deposit_runs DIRECT, 128-bit loads);
+    // fp64 or unaligned: warp runs (k_deposit_warp).  Measured on 10^7 sorted
+    // particles, 64^3 grid: fp32 11.0 (lane) vs 13.2 ps (warp), fp64 34.0 vs 22.5 ps.
+    if constexpr (sizeof(FP) == 4) {
         auto al16 = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
-        const bool direct = sizeof(FP) == 4 && deposit_direct_enabled() && al16(e.soa.x) &&
-                            al16(e.soa.y) && al16(e.soa.z) && al16(e.soa.px) &&
-                            al16(e.soa.py) && al16(e.soa.pz) && al16(e.soa.w) &&
-                            al16(e.soa.type);
-        if constexpr (sizeof(FP) == 4) {
-            if (direct) {
-                const int64_t blocks = (tiles + 7) / 8;
-                const unsigned grid = (unsigned)stream_grid(blocks, 4, device);
-                k_deposit_runs<FP, true><<<grid, 8 * 32, 0, st>>>(e, g, dc, (FP *)Jx,
-                                                                   (FP *)Jy, (FP *)Jz);
-                return cudaGetLastError();
-            }
+        if (e.layout == BORIS_LAYOUT_SOA && al16(e.soa.x) && al16(e.soa.y) && al16(e.soa.z) &&
+            al16(e.soa.px) && al16(e.soa.py) && al16(e.soa.pz) && al16(e.soa.w) &&
+            al16(e.soa.type)) {
+            using R = DepRuns<FP>;
+            const int64_t tiles = (e.n + R::TILE - 1) / R::TILE;
+            const int64_t blocks = (tiles + 7) / 8;
+            const unsigned grid = (unsigned)stream_grid(blocks, 4, device);
+            k_deposit_runs<FP, true><<<grid, 8 * 32, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy,
+                                                               (FP *)Jz);
+            return cudaGetLastError();
         }
-        const int64_t blocks = (tiles + R::WARPS - 1) / R::WARPS;
-        const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
-        k_deposit_runs<FP, false><<<grid, R::WARPS * 32, 0, st>>>(e, g, dc, (FP *)Jx,
-                                                                   (FP *)Jy, (FP *)Jz);
+    }
+    if (e.layout == BORIS_LAYOUT_SOA) {
+        // one contiguous chunk per warp, a multiple of 32 particles, sized so the
+        // resident blocks cover the ensemble in one wave
+        using D = DepWarp<FP>;
+        const int64_t warps = (int64_t)sm_count(device) * D::MINB * D::WARPS;
+        int64_t chunk = (e.n + warps - 1) / warps;
+        chunk = (chunk + 31) / 32 * 32;
+        const int64_t blocks = ((e.n + chunk - 1) / chunk + D::WARPS - 1) / D::WARPS;
+        const bool multi = dc.n_types > 1 && e.soa.type;
+        if (multi)
+            k_deposit_warp<FP, true><<<(unsigned)blocks, D::WARPS * 32, 0, st>>>(
+                e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz, chunk);
+        else
+            k_deposit_warp<FP, false><<<(unsigned)blocks, D::WARPS * 32, 0, st>>>(
+                e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz, chunk);
         return cudaGetLastError();
     }
     const int64_t blocks = (e.n + 255) / 256;

@@ -208,18 +208,6 @@ static cudaError_t dispatch_soa_grid(const EnsView &e, const GridArgs<FP> &g,
 
 static bool aligned16(const void *p);
 
-// Grid single-step kernel: "tma" (k_stream_soa_grid_tma, state staged by bulk
-// copies) or "ldg" (k_stream_soa_grid); BORIS_GRID_KERNEL overrides the default.
-// Both are bitwise identical.
-static bool use_tma_grid() {
-    static int v = -1;
-    if (v < 0) {
-        const char *s = getenv("BORIS_GRID_KERNEL");
-        v = (s && s[0] == 't') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 // Returns cudaErrorNotSupported when the arrays are not 16 B aligned (the caller
 // then uses the fused kernel).
 template <typename FP>
@@ -235,8 +223,6 @@ cudaError_t launch_stream_soa_grid(const EnsView &e, const GridArgs<FP> &g, cons
                     aligned16(e.soa.g) && (!diag || !e.soa.w || aligned16(e.soa.w)) &&
                     (!multi || ((uintptr_t)e.soa.type & (2 * V - 1)) == 0);
     if (!al) return cudaErrorNotSupported;
-    if (use_tma_grid() && (!multi || aligned16(e.soa.type)))
-        return launch_stream_soa_grid_tma<FP>(e, g, co, multi, diag, device, st);
     const bool d = diag != nullptr;
     if (multi)
         return d ? dispatch_soa_grid<FP, true, true>(e, g, co, diag, device, st)
@@ -441,18 +427,6 @@ __global__ void __launch_bounds__(kStreamThreads)
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
-// Tuning: BORIS_STREAM_GRID=<blocks> overrides the grid of the vector streaming
-// kernel (experiments on grid size under the board power cap; 0/unset: default).
-static int64_t stream_grid_override() {
-    static int64_t v = -1;
-    if (v < 0) {
-        const char *s = getenv("BORIS_STREAM_GRID");
-        v = s ? atoll(s) : 0;
-        if (v < 0) v = 0;
-    }
-    return v;
-}
-
 template <typename FP, bool MULTI, bool DIAG>
 static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
                                 DiagOut *diag, int device, cudaStream_t st) {
@@ -469,8 +443,6 @@ static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const C
         const int64_t n_groups = e.n / V;
         const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
         grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
-        if (stream_grid_override() > 0 && stream_grid_override() < grid)
-            grid = stream_grid_override();
         if (DIAG && grid > diag->cap) grid = diag->cap;
         k_stream_soa_vec<FP, MULTI, DIAG>
             <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, co, n_groups, e.n, partials);
@@ -485,32 +457,12 @@ static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const C
     return cudaGetLastError();
 }
 
-// Kernel selection for SoA streaming: "ldg" (default, k_stream_soa_vec) or "tma"
-// (k_stream_soa_tma); BORIS_SOA_KERNEL overrides.  Both are bitwise identical.
-static bool use_tma_soa() {
-    static int v = -1;
-    if (v < 0) {
-        const char *s = getenv("BORIS_SOA_KERNEL");
-        v = (s && s[0] == 't') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 template <typename FP>
 cudaError_t launch_stream_soa(const EnsView &e, const FieldSoaPtrs &f, const Coefs<FP> &co,
                               bool multi, DiagOut *diag, int device, cudaStream_t st) {
     if (e.n == 0) {
         if (diag) diag->written = 0;
         return cudaSuccess;
-    }
-    if (use_tma_soa()) {
-        const bool al = aligned16(e.soa.x) && aligned16(e.soa.y) && aligned16(e.soa.z) &&
-                        aligned16(e.soa.px) && aligned16(e.soa.py) && aligned16(e.soa.pz) &&
-                        aligned16(e.soa.g) && aligned16(f.Ex) && aligned16(f.Ey) &&
-                        aligned16(f.Ez) && aligned16(f.Bx) && aligned16(f.By) &&
-                        aligned16(f.Bz) && (!diag || !e.soa.w || aligned16(e.soa.w)) &&
-                        (!multi || aligned16(e.soa.type));
-        if (al) return launch_stream_soa_tma<FP>(e, f, co, multi, diag, device, st);
     }
     const bool d = diag != nullptr;
     if (multi)

@@ -152,11 +152,11 @@ def main():
     rows.append(fused("C4-soa-fp32-planewave-100", "C4", "soa", "fp32", n1, 100))
     rows.append(fused("C4-soa-fp64-planewave-100", "C4", "soa", "fp64", n1 // 4, 100))
     # the same two C4 rows and C3 through the generic (any-orientation) fused kernel
-    os.environ["BORIS_FUSED_GENERIC"] = "1"
+    lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 1)
     rows.append(fused("C3-aos-fp64-crossed-100-generic", "C3", "aos", "fp64", 10_000_000, 100))
     rows.append(fused("C4-soa-fp32-planewave-100-generic", "C4", "soa", "fp32", n1, 100))
     rows.append(fused("C4-soa-fp64-planewave-100-generic", "C4", "soa", "fp64", n1 // 4, 100))
-    del os.environ["BORIS_FUSED_GENERIC"]
+    lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 0)
     rows.append(fused("mdipole-soa-fp32-100", "C4", "soa", "fp32", n1 // 4, 100,
                       field_kind="mdipole"))
     rows.append(fused("mdipole-soa-fp64-100", "C4", "soa", "fp64", n1 // 10, 100,

@@ -111,18 +111,18 @@ def main():
                     f = analytic("plane_wave")
                     lb.boris_push_ex(e.handle, f, w.dt, 2, flags, dp)
                     lb.boris_field_destroy(f)
-                for generic in ("0", "1"):   # axis-aligned specialisation and generic
-                    os.environ["BORIS_FUSED_GENERIC"] = generic
+                for generic in (0, 1):   # axis-aligned specialisation and generic
+                    lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, generic)
                     for kind in ("uniform", "plane_wave"):
                         f = analytic(kind)
                         lb.boris_push_diag(e.handle, f, w.dt, 11, dp)
                         lb.boris_field_destroy(f)
-                os.environ.pop("BORIS_FUSED_GENERIC")
+                lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 0)
                 torch.cuda.synchronize()
                 e.close()
         lb.boris_field_destroy(grid)
     # host-resident pipeline, several chunks
-    os.environ["BORIS_HOST_CHUNK"] = "2048"
+    lb.boris_set_option(lb.BORIS_OPT_HOST_CHUNK, 2048)
     w = synth.config("C5", n=5000)
     for cls in (SoaEnsemble, AosEnsemble):
         e = cls(w.n, lb.BORIS_FP32, w.types, w.light_velocity, host=True)

@@ -108,9 +108,13 @@ class Displacement:
       (each fl(r^n) errs by <= u |r^n|; |r^n| <= |r0| + path).  A is what any FP-storage
       implementation incurs; for fp32 single steps it dominates;
     * ensemble bias: b = sum_i (dr_gpu - dr_ref).dr_ref / sum_i |dr_ref|^2, the relative
-      scale error of the GPU's displacements.  Storage rounding is unbiased and averages
-      out (noise ~ A/(|dr| sqrt(n))), a systematic error in a10 (e.g. a wrong dt/(S m))
-      does not: |b| <= tol.
+      scale error of the GPU's displacements.  Storage rounding does not average to zero
+      exactly: each particle contributes at most A_i |dr_i| to the numerator with an
+      input-dependent sign, so b carries rounding noise up to
+      N_b = 5 sqrt(sum_i (A_i |dr_i|)^2) / sum_i |dr_i|^2 (5 sigma for independent
+      signs; it matters when |dr| is a few ulp of |r|, e.g. particles 2 steps from rest).
+      A systematic error in a10 (e.g. a wrong dt/(S m)) does not average out:
+      |b| - N_b <= tol.  The second value returned is sign(b) max(|b| - N_b, 0).
     """
 
     def __init__(self, r0, precision):
@@ -132,4 +136,7 @@ class Displacement:
         err = np.maximum(np.linalg.norm(diff, axis=1) - allow, 0.0) / (nrm + s)
         den = float(np.sum(dr * dr))
         bias = float(np.sum(diff * dr)) / den if den > 0 else 0.0
-        return (float(err.max()) if err.size else 0.0), bias
+        noise = 5.0 * float(np.sqrt(np.sum((allow * nrm) ** 2))) / den if den > 0 else 0.0
+        self.last_bias, self.last_noise = bias, noise
+        excess = np.sign(bias) * max(abs(bias) - noise, 0.0)
+        return (float(err.max()) if err.size else 0.0), float(excess)

@@ -41,6 +41,21 @@ def gpu_field(w):
     return None
 
 
+@pytest.fixture
+def boris_option():
+    """Set a process-wide library option (boris_set_option) for one test; the
+    previous value is restored afterwards."""
+    saved = {}
+
+    def set_(opt, value):
+        saved.setdefault(opt, lb.boris_get_option(opt))
+        lb.boris_set_option(opt, value)
+
+    yield set_
+    for opt, value in saved.items():
+        lb.boris_set_option(opt, value)
+
+
 def build(w, layout, precision, n=None, host=False):
     n = n or w.n
     d = rounded(w.generate(0, n), precision)
@@ -323,15 +338,15 @@ def test_plane_wave_other_orientations_parity(orient):
 @pytest.mark.parametrize("cfg,layout,precision", [("C4", "soa", "fp32"), ("C4", "aos", "fp64"),
                                                   ("C3", "aos", "fp64"), ("C3", "soa", "fp32"),
                                                   ("C1", "soa", "fp64")])
-def test_axis_aligned_specialisation_equals_generic_bitwise(cfg, layout, precision, monkeypatch):
+def test_axis_aligned_specialisation_equals_generic_bitwise(cfg, layout, precision, boris_option):
     """k_fused's YZ specialisation (E || y, B || z: C1, C3, C4) drops only products with
-    exact zeros, so it equals the generic kernel bitwise (BORIS_FUSED_GENERIC=1)."""
+    exact zeros, so it equals the generic kernel bitwise (BORIS_OPT_FUSED_GENERIC = 1)."""
     w = synth.config(cfg)
     n = w.n if cfg == "C1" else N_SMALL
     steps = 37
     states = []
-    for generic in ("0", "1"):
-        monkeypatch.setenv("BORIS_FUSED_GENERIC", generic)
+    for generic in (0, 1):
+        boris_option(lb.BORIS_OPT_FUSED_GENERIC, generic)
         _, ens, f = build(w, layout, precision, n)
         diag = torch.zeros(2, dtype=torch.float64, device="cuda")
         lb.boris_push_diag(ens.handle, f, w.dt, steps, diag.data_ptr())
@@ -394,6 +409,76 @@ def test_mdipole_parity(precision):
     w = mdipole_workload()
     worst = run_parity(w, "soa", precision, N_SMALL, checks=(1, 2, 10, 100))
     print(precision, worst)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_mdipole_beyond_time_table_one_call(precision):
+    """1500 m-dipole steps in ONE boris_push_diag call: the fused kernel's per-block
+    time tables hold 1024 steps, so the call runs as several launches (t0 shifted,
+    the position anchor rounded to FP between them, the diagnostic on the last).
+    Against the oracle (c15 metric, eq. 14 in readings c9-c13), plus KE and count."""
+    w = mdipole_workload()
+    n = 2048 + 13
+    d, ens, field = build(w, "soa", precision, n)
+    ref = OracleRun(w, d, precision)
+    steps = 1500
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_diag(ens.handle, field, w.dt, steps, diag.data_ptr())
+    ref.push(steps)
+    torch.cuda.synchronize()
+    r, p, g, st = gpu_state(ens)
+    metric = C15()
+    er, ep = metric("r", r, ref.pos), metric("p", p, ref.mom)
+    print(precision, er, ep)
+    # north_star's bar holds "after 100 steps"; rounding errors of independent steps
+    # add as a random walk, so 1500 steps get sqrt(1500/100) times the bar (measured
+    # fp32: 1.2e-5 for p, 3e-7 for r; fp64 within the plain 1e-12)
+    tol = TOL[precision] * (math.sqrt(steps / 100) if precision == "fp32" else 1.0)
+    assert er <= tol and ep <= tol, (er, ep)
+    assert lb.boris_ensemble_get_time(ens.handle) == pytest.approx(steps * w.dt, rel=1e-15)
+    assert diag[1].item() == n
+    ke = ref.kinetic_energy()
+    assert abs(diag[0].item() - ke) <= 10 * tol * abs(ke), (diag[0].item(), ke)
+    lb.boris_field_destroy(field)
+    ens.close()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_field_evaluate_mdipole_is_the_fused_step_field(precision):
+    """boris_field_evaluate returns the field the fused push uses (libboris.h): one
+    streaming step with the evaluated m-dipole arrays gives bitwise the momenta and
+    gamma of one fused m-dipole step from the same state at the same time (both
+    branches of reading c13 occur: xi = kR spans 0..3.8 in the 0.6 lambda sphere)."""
+    w = mdipole_workload()
+    n = N_SMALL
+    d = rounded(w.generate(0, n), precision)
+    g = torch.Generator().manual_seed(11)
+    for k in ("px", "py", "pz"):   # moving particles: the rotation is exercised
+        d[k] = rounded({k: 3.0 * synth.M_ELECTRON * synth.C_LIGHT
+                        * torch.randn(n, generator=g, dtype=torch.float64)}, precision)[k]
+    t0 = 0.29 * synth.T0
+    a = SoaEnsemble(n, PREC[precision], w.types, w.light_velocity, with_fields=True)
+    b = SoaEnsemble(n, PREC[precision], w.types, w.light_velocity, with_fields=False)
+    for e in (a, b):
+        e.fill(d)
+        e.wrap()
+        lb.boris_ensemble_set_time(e.handle, t0)
+    src = gpu_field(w)
+    lb.boris_field_evaluate(src, a.handle, t0, a.field)
+    lb.boris_push_ex(a.handle, a.field, w.dt, 1, lb.BORIS_PUSH_STREAM_EACH_STEP)
+    lb.boris_push(b.handle, src, w.dt, 1)
+    torch.cuda.synchronize()
+    sa, sb = a.state(), b.state()
+    for k in ("px", "py", "pz", "gamma"):
+        assert torch.equal(sa[k], sb[k]), k
+    # positions: r + dt v in one FMA (streaming) vs fp64 anchor + FP displacement (fused)
+    for k in ("x", "y", "z"):
+        ulp = np.spacing(np.abs(sb[k].numpy()).astype(np.float32 if precision == "fp32"
+                                                      else np.float64))
+        assert np.all(np.abs(sa[k].numpy() - sb[k].numpy()) <= ulp), k
+    lb.boris_field_destroy(src)
+    a.close()
+    b.close()
 
 
 @pytest.mark.parametrize("kind", ["uniform", "plane_wave", "mdipole"])
@@ -499,8 +584,8 @@ def test_upload_download_roundtrip(layout, precision):
 
 
 @pytest.mark.parametrize("layout", ["soa", "aos"])
-def test_host_resident_equals_device_bitwise(layout, monkeypatch):
-    monkeypatch.setenv("BORIS_HOST_CHUNK", "4096")  # several chunks through the pipeline
+def test_host_resident_equals_device_bitwise(layout, boris_option):
+    boris_option(lb.BORIS_OPT_HOST_CHUNK, 4096)  # several chunks through the pipeline
     w = synth.config("C2")
     _, dev, fdev = build(w, layout, "fp32", N_SMALL)
     _, host, fhost = build(w, layout, "fp32", N_SMALL, host=True)
