@@ -326,8 +326,10 @@ boris_status boris_push_deposit(boris_ensemble *ens, const boris_field *grid, do
  * position r_i at time t and write it into the per-particle field `out` (arrays
  * created with boris_field_create_arrays_* for `ens`; layout, precision, n,
  * device and residency must match, else MISMATCH).  The values are those the
- * fused push would use at (r_i, t) (the same arithmetic).  Device ensembles
- * only.  Asynchronous.
+ * fused push uses at (r_i, t), to rounding: the m-dipole is evaluated with the
+ * fused step's radial functions and branch (reading c13), but the single-type
+ * Boris fused push folds the type's coefficients into the field's scalar
+ * factors instead of forming E and B.  Device ensembles only.  Asynchronous.
  */
 boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensemble *ens,
                                   double t, const boris_field *out, void *stream);

@@ -402,12 +402,20 @@ __global__ void __launch_bounds__(kFusedThreads)
     __shared__ FP s_sin[FIELD == FK_MDIPOLE ? kTimeTab : 1];
     __shared__ FP s_cos[FIELD == FK_MDIPOLE ? kTimeTab : 1];
     if (MULTI) load_type_table(co, s_t);
+    // single-type Boris m-dipole: the type's half-kick and rotation factors are folded
+    // into the time tables (kMdFold: t and the kick come straight from the field's
+    // scalar factors, no E, B vectors are formed)
+    constexpr bool kMdFold = FIELD == FK_MDIPOLE && !MULTI && PUSHER == PUSHER_BORIS;
     if constexpr (FIELD == FK_MDIPOLE) {
         for (int j = threadIdx.x; j < n_steps; j += kFusedThreads) {
             double sn, cs;
             sincos(fa.w0t0 + (double)j * fa.w0dt, &sn, &cs);  // t_j = t0 + j dt (c5)
             s_sin[j] = b_mul(fa.mA02, (FP)sn);   // -2 A0 sin(w t_j)
             s_cos[j] = b_mul(fa.A0k2, (FP)cs);   // 2 A0 k cos(w t_j)
+            if (kMdFold) {
+                s_sin[j] = b_mul(co.t[0].alpha, s_sin[j]);  // alpha (-2 A0 sin)
+                s_cos[j] = b_mul(co.t[0].aE, s_cos[j]);     // aE (2 A0 k cos)
+            }
         }
         __syncthreads();
     }
@@ -506,6 +514,26 @@ __global__ void __launch_bounds__(kFusedThreads)
                                     b_add((FP)za, dz), Ex, Ey, Ez, Bx, By, Bz);
 #endif
                     inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
+                } else if constexpr (kMdFold) {  // eq. 14 (c9, c10, c13), factors folded
+                    // E = ce g1 (-y, x, 0), B = sb (k^2 g2 z r + f3 z^); the kick is
+                    // aE E = e (-y, x, 0) with e = (aE ce) g1, and the rotation vector
+                    // t = alpha B / gamma_n = a r + b z^ with a = (alpha sb / gamma_n) k^2 g2 z,
+                    // b = (alpha sb / gamma_n) f3 (eq. 9-13; E_z = 0 exactly)
+                    const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
+                    FP g1, g2, f3;
+                    md_radial_r2<FP>(fa, b_norm2(x, y, z), g1, g2, f3);
+                    const FP e = b_mul(s_cos[s0 + j], g1);
+                    ux = b_fma(-e, y, ux);
+                    uy = b_fma(e, x, uy);
+                    const FP tsb = b_mul(s_sin[s0 + j], b_rsqrt(b_fma(tc.kappa2,
+                                                                      b_norm2(ux, uy, uz), FP(1))));
+                    const FP al = b_mul(tsb, b_mul(b_mul(fa.k2, g2), z));
+                    boris_rotate<FP>(ux, uy, uz, b_mul(al, x), b_mul(al, y),
+                                     b_fma(al, z, b_mul(tsb, f3)));
+                    ux = b_fma(-e, y, ux);
+                    uy = b_fma(e, x, uy);
+                    // gamma^{n+1/2} is stored once after the loop (same operations)
+                    inv_g = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
@@ -550,6 +578,7 @@ __global__ void __launch_bounds__(kFusedThreads)
         }
         const double x = xa, y = ya, z = za;
         if (n_steps == 0) gam = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
+        else if (kMdFold) boris_gamma<FP>(ux, uy, uz, tc.kappa2, gam);
         Particle<FP, LAYOUT>::store(e, i, x, y, z, b_mul(ux, tc.invS), b_mul(uy, tc.invS),
                                     b_mul(uz, tc.invS), gam);
         if (DIAG) {

@@ -119,6 +119,12 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
 #define BORIS_GRID_MINB 3
 #endif
 #define BORIS_GRID_BOUNDS __launch_bounds__(kStreamThreads, BORIS_GRID_MINB)
+#ifndef BORIS_GRID_REUSE
+#define BORIS_GRID_REUSE 0
+#endif
+#ifndef BORIS_GRID_PREFETCH
+#define BORIS_GRID_PREFETCH 0
+#endif
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void BORIS_GRID_BOUNDS
     k_stream_soa_grid(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
@@ -132,47 +138,74 @@ __global__ void BORIS_GRID_BOUNDS
     const FP *W = (const FP *)s.w;
     double ke = 0.0, cnt = 0.0;
     const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
-    for (int64_t grp = (int64_t)blockIdx.x * kStreamThreads + threadIdx.x; grp < n_groups;
-         grp += stride) {
-        const int64_t i0 = grp * V;
-        Vec<FP> x, y, z, px, py, pz, w, gm;
-        x.load_state(X + i0);
-        y.load_state(Y + i0);
-        z.load_state(Z + i0);
-        px.load_state(PX + i0);
-        py.load_state(PY + i0);
-        pz.load_state(PZ + i0);
+#if BORIS_GRID_REUSE
+    GridCache<FP> gcache;  // consecutive (sorted: same-cell) particles reuse the records
+#endif
+    struct State {
+        Vec<FP> x, y, z, px, py, pz, w;
         int ty[V];
-        if (MULTI) load_types<V>(s.type + i0, ty);
+    };
+    auto load = [&](int64_t grp, State &st) {
+        const int64_t i0 = grp * V;
+        st.x.load_state(X + i0);
+        st.y.load_state(Y + i0);
+        st.z.load_state(Z + i0);
+        st.px.load_state(PX + i0);
+        st.py.load_state(PY + i0);
+        st.pz.load_state(PZ + i0);
+        if (MULTI) load_types<V>(s.type + i0, st.ty);
         if (DIAG) {
-            if (W) w.load_field(W + i0);
+            if (W) st.w.load_field(W + i0);
             else {
 #pragma unroll
-                for (int j = 0; j < V; ++j) w.v[j] = FP(1);
+                for (int j = 0; j < V; ++j) st.w.v[j] = FP(1);
             }
         }
+    };
+    int64_t grp = (int64_t)blockIdx.x * kStreamThreads + threadIdx.x;
+    State cur;
+    if (grp < n_groups) load(grp, cur);
+    for (; grp < n_groups; grp += stride) {
+        const int64_t i0 = grp * V;
+#if BORIS_GRID_PREFETCH
+        State nxt;
+        if (grp + stride < n_groups) load(grp + stride, nxt);
+#endif
+        Vec<FP> gm;
         FP ex[V], ey[V], ez[V], bx[V], by[V], bz[V];
 #pragma unroll
         for (int j = 0; j < V; ++j)
-            grid_gather<FP>(g, x.v[j], y.v[j], z.v[j], ex[j], ey[j], ez[j], bx[j], by[j], bz[j]);
+#if BORIS_GRID_REUSE
+            grid_gather_cached<FP>(g, cur.x.v[j], cur.y.v[j], cur.z.v[j], gcache, ex[j], ey[j],
+                                   ez[j], bx[j], by[j], bz[j]);
+#else
+            grid_gather<FP>(g, cur.x.v[j], cur.y.v[j], cur.z.v[j], ex[j], ey[j], ez[j], bx[j],
+                            by[j], bz[j]);
+#endif
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const TypeCoef<FP> tc = MULTI ? s_t[ty[j]] : co.t[0];
+            const TypeCoef<FP> tc = MULTI ? s_t[cur.ty[j]] : co.t[0];
             FP ux, uy, uz;
-            push_one<FP>(x.v[j], y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], gm.v[j], ex[j], ey[j],
-                         ez[j], bx[j], by[j], bz[j], tc, ux, uy, uz);
+            push_one<FP>(cur.x.v[j], cur.y.v[j], cur.z.v[j], cur.px.v[j], cur.py.v[j],
+                         cur.pz.v[j], gm.v[j], ex[j], ey[j], ez[j], bx[j], by[j], bz[j], tc, ux,
+                         uy, uz);
             if (DIAG) {
-                ke += (double)kinetic_energy<FP>(ux, uy, uz, gm.v[j], w.v[j], tc);
+                ke += (double)kinetic_energy<FP>(ux, uy, uz, gm.v[j], cur.w.v[j], tc);
                 cnt += 1.0;
             }
         }
-        x.store(X + i0);
-        y.store(Y + i0);
-        z.store(Z + i0);
-        px.store(PX + i0);
-        py.store(PY + i0);
-        pz.store(PZ + i0);
+        cur.x.store(X + i0);
+        cur.y.store(Y + i0);
+        cur.z.store(Z + i0);
+        cur.px.store(PX + i0);
+        cur.py.store(PY + i0);
+        cur.pz.store(PZ + i0);
         gm.store(G + i0);
+#if BORIS_GRID_PREFETCH
+        cur = nxt;
+#else
+        if (grp + stride < n_groups) load(grp + stride, cur);
+#endif
     }
     const int64_t tail0 = n_groups * V;
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail0) {
