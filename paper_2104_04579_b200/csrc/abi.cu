@@ -1155,7 +1155,8 @@ static DepCoefs<FP> make_dep_coefs(const boris_ensemble *e, const boris_field *g
         const double q = e->types[i].charge, m = e->types[i].mass, mc = m * e->c;
         const double S = std::ldexp(1.0, -(int)std::lround(std::log2(mc)));
         dc.t[i].S = (FP)S;
-        dc.t[i].kappa2 = (FP)(1.0 / ((S * mc) * (S * mc)));
+        const double kappa = 1.0 / (S * mc);  // as make_coefs: the fused PIC step reuses
+        dc.t[i].kappa2 = (FP)(kappa * kappa);  // the push's 1/gamma bitwise
         dc.t[i].inv_Sm = (FP)(1.0 / (S * m));
         dc.t[i].q_vol = (FP)(q / vol);
     }

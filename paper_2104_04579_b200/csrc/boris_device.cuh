@@ -361,8 +361,9 @@ __device__ __forceinline__ FP momentum_update(FP &ux, FP &uy, FP &uz, FP Ex, FP 
 // One full Boris step of one particle on stored quantities (rows a1-a11):
 // p -> u (exact), boris_momentum, position update, u -> p (exact).  Shared by
 // every streaming path so they are bitwise identical.
+// Returns 1/gamma^{n+1/2} (the deposition's v = u inv_Sm / gamma reuses it).
 template <typename FP, int PUSHER = PUSHER_BORIS>
-__device__ __forceinline__ void push_one(FP &x, FP &y, FP &z, FP &px, FP &py, FP &pz, FP &g,
+__device__ __forceinline__ FP push_one(FP &x, FP &y, FP &z, FP &px, FP &py, FP &pz, FP &g,
                                          FP Ex, FP Ey, FP Ez, FP Bx, FP By, FP Bz,
                                          const TypeCoef<FP> &tc, FP &ux, FP &uy, FP &uz) {
     ux = b_mul(px, tc.S);
@@ -378,6 +379,7 @@ __device__ __forceinline__ void push_one(FP &x, FP &y, FP &z, FP &px, FP &py, FP
     px = b_mul(ux, tc.invS);
     py = b_mul(uy, tc.invS);
     pz = b_mul(uz, tc.invS);
+    return inv_g;
 }
 
 // Kinetic energy of one macroparticle, w m c^2 |p/(mc)|^2 / (gamma + 1)

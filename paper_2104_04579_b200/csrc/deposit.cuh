@@ -14,6 +14,21 @@ namespace boris {
 
 constexpr uint32_t kNoNode = 0xFFFFFFFFu;
 
+// End-of-tile merge of the lanes' open cells: shuffle scan (warp_merge + flush) or
+// transposed through shared memory (merge_flush; fp32 only, fp64's 24 x 34 doubles
+// per warp would exceed static shared memory).  Standalone deposition (kTransposedMerge)
+// and the fused PIC step (kTransposedMergePD) choose separately (measured).
+#ifndef BORIS_DEP_MERGE_T
+#define BORIS_DEP_MERGE_T 0
+#endif
+#ifndef BORIS_PD_MERGE_T
+#define BORIS_PD_MERGE_T 1
+#endif
+template <typename FP>
+constexpr bool kTransposedMerge = sizeof(FP) == 4 && BORIS_DEP_MERGE_T;
+template <typename FP>
+constexpr bool kTransposedMergePD = sizeof(FP) == 4 && BORIS_PD_MERGE_T;
+
 template <typename FP>
 struct DepositRun {
     FP acc[8][3];
@@ -72,8 +87,17 @@ struct DepositRun {
                                         FP x, FP y, FP z, FP px, FP py, FP pz, FP w, FP *Jx,
                                         FP *Jy, FP *Jz) {
         const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
+        add_u(g, t, half_dt, x, y, z, ux, uy, uz,
+              b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))), w, Jx, Jy, Jz);
+    }
+
+    // The same with u = S p and 1/gamma known (the fused PIC step has both from the
+    // push: bitwise the values add() recomputes).
+    __device__ __forceinline__ void add_u(const GridArgs<FP> &g, const DepCoef<FP> &t, FP half_dt,
+                                          FP x, FP y, FP z, FP ux, FP uy, FP uz, FP inv_g, FP w,
+                                          FP *Jx, FP *Jy, FP *Jz) {
         // v = p/(gamma m) = u/(S m gamma)
-        const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
+        const FP vf = b_mul(t.inv_Sm, inv_g);
         const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
         FP fx, fy, fz;
         const FP lx = axis_floor(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], fx);
@@ -106,6 +130,79 @@ struct DepositRun {
                     acc[q][2] = b_fma(sw, vz, acc[q][2]);
                 }
             }
+    }
+
+    // Per-warp scratch of merge_flush.
+    struct MergeSmem {
+        static constexpr int RS = sizeof(FP) == 4 ? 36 : 34;  // row stride: conflict-free
+        FP red[24 * RS];      // red[t * RS + l] = lane l's sum t = q * 3 + d
+        uint32_t rowb[4][32];  // lane l's open cell: row bases ((k*ny + j)*nx) for (b, c)
+        int cxs[2][32];        // and its two x node indices
+    };
+
+    // End of a warp tile (all 32 lanes), transposed: every lane stashes its 24 sums
+    // in shared memory, then lane t < 24 walks component t of the 32 lanes in lane
+    // order and adds each run of equal open cells (contiguous when sorted) to J
+    // with one atomic at the run's last lane -- one 24-lane atomic instruction per
+    // run instead of a shuffle scan over the 24 sums.  The run ends (tails) are
+    // warp-uniform, so the walk's branches do not diverge.
+    __device__ __forceinline__ void merge_flush(const GridArgs<FP> &g, FP *Jx, FP *Jy, FP *Jz,
+                                                MergeSmem &sm, int lane) {
+        const unsigned full = 0xffffffffu;
+        const bool has = cx[0] >= 0;
+        const uint32_t key = has ? ((uint32_t)cz[0] * (uint32_t)g.n[1] + (uint32_t)cy[0]) *
+                                           (uint32_t)g.n[0] + (uint32_t)cx[0]
+                                 : kNoNode;
+        const uint32_t next = __shfl_down_sync(full, key, 1);
+        const unsigned tails = __ballot_sync(full, has && (lane == 31 || next != key));
+        if (tails == 0) return;
+        constexpr int RS = MergeSmem::RS;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                sm.red[(q * 3 + d) * RS + lane] = acc[q][d];
+                acc[q][d] = FP(0);
+            }
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+                sm.rowb[c * 2 + b][lane] =
+                    ((uint32_t)cz[c] * (uint32_t)g.n[1] + (uint32_t)cy[b]) * (uint32_t)g.n[0];
+        sm.cxs[0][lane] = cx[0];
+        sm.cxs[1][lane] = cx[1];
+        cx[0] = -1;
+        __syncwarp();
+        if (lane < 24) {
+            const int q = lane / 3, d = lane - 3 * (lane / 3);
+            FP *J = d == 0 ? Jx : (d == 1 ? Jy : Jz);
+            const FP *row = sm.red + lane * RS;
+            const uint32_t *rb = sm.rowb[q >> 1];
+            const int *xs = sm.cxs[q & 1];
+            FP run = FP(0);
+            constexpr int VW = 16 / sizeof(FP);  // FP per 16 B vector
+#pragma unroll
+            for (int l0 = 0; l0 < 32; l0 += VW) {
+                FP v[VW];
+                if constexpr (VW == 4) {
+                    const float4 t = reinterpret_cast<const float4 *>(row)[l0 / 4];
+                    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+                } else {
+                    const double2 t = reinterpret_cast<const double2 *>(row)[l0 / 2];
+                    v[0] = t.x; v[1] = t.y;
+                }
+#pragma unroll
+                for (int k = 0; k < VW; ++k) {
+                    run = b_add(run, v[k]);
+                    if (tails & (1u << (l0 + k))) {  // warp-uniform
+                        atomicAdd(J + rb[l0 + k] + (uint32_t)xs[l0 + k], run);
+                        run = FP(0);
+                    }
+                }
+            }
+        }
+        __syncwarp();
     }
 
     // End of a warp tile (all 32 lanes): lanes holding the same open cell in

@@ -608,6 +608,7 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
     constexpr int NW = DIRECT ? 8 : R::WARPS;
     __shared__ FP s[DIRECT ? 1 : R::WARPS][7][DIRECT ? 1 : R::SK];
     __shared__ int16_t s_ty[DIRECT ? 1 : R::WARPS][DIRECT ? 1 : R::SK];
+    __shared__ typename DepositRun<FP>::MergeSmem s_merge[DIRECT && kTransposedMerge<FP> ? 8 : 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const FP *arr[7] = {(const FP *)e.soa.x, (const FP *)e.soa.y, (const FP *)e.soa.z,
                         (const FP *)e.soa.px, (const FP *)e.soa.py, (const FP *)e.soa.pz,
@@ -706,9 +707,13 @@ __global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
             const DepCoef<FP> t = dc.t[multi ? (DIRECT ? rty[j] : s_ty[warp][sp]) : 0];
             run.add(g, t, dc.half_dt, x, y, z, px, py, pz, w, Jx, Jy, Jz);
         }
-        // end of tile: merge lanes holding the same cell, one flush per segment
-        run.warp_merge(g, lane);
-        run.flush(g, Jx, Jy, Jz);
+        // end of tile: merge lanes holding the same cell, one atomic per segment
+        if constexpr (DIRECT && kTransposedMerge<FP>) {
+            run.merge_flush(g, Jx, Jy, Jz, s_merge[warp], lane);
+        } else {
+            run.warp_merge(g, lane);
+            run.flush(g, Jx, Jy, Jz);
+        }
         __syncwarp();
     }
 }

@@ -290,6 +290,8 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
     constexpr int V = Vec<FP>::N;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     __shared__ DepCoef<FP> s_d[MULTI ? kMaxTypes : 1];
+    __shared__ typename DepositRun<FP>::MergeSmem
+        s_merge[kTransposedMergePD<FP> ? kStreamThreads / 32 : 1];
     if (MULTI) {
         for (int k = threadIdx.x; k < dc.n_types; k += blockDim.x) s_d[k] = dc.t[k];
         load_type_table(co, s_t);  // ends with __syncthreads
@@ -345,13 +347,19 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             py.store(PY + i0);
             pz.store(PZ + i0);
             gm.store(G + i0);
+            // deposition of the new state (measured: recomputing 1/gamma from the
+            // stored p after the stores beats carrying the push's u and 1/gamma)
 #pragma unroll
             for (int j = 0; j < V; ++j)
                 run.add(g, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j], y.v[j], z.v[j],
                         px.v[j], py.v[j], pz.v[j], w.v[j], Jx, Jy, Jz);
         }
-        run.warp_merge(g, lane);
-        run.flush(g, Jx, Jy, Jz);
+        if constexpr (kTransposedMergePD<FP>) {
+            run.merge_flush(g, Jx, Jy, Jz, s_merge[threadIdx.x >> 5], lane);
+        } else {
+            run.warp_merge(g, lane);
+            run.flush(g, Jx, Jy, Jz);
+        }
     }
     // ragged tail (n mod V particles): push then deposit directly
     const int64_t tail0 = n_groups * V;
