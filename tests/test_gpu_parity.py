@@ -1075,6 +1075,60 @@ def test_sort_by_cell_is_a_stable_permutation(precision, layout):
     ens.close()
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("has_w,has_type", [(True, False), (False, False), (False, True),
+                                            (True, True)])
+def test_sort_wrapped_arrays_with_optional_components(precision, has_w, has_type):
+    """boris_ensemble_sort_by_cell on wrapped torch arrays with weight / type absent
+    (NULL) or present, one element off 16 B alignment: every record layout of the
+    permutation (packed records of 7-8 FP slots + an optional type slot, vector or
+    shared-memory packing) moves each particle whole and sorts by cell (PAPER.md
+    L233-236)."""
+    h, params, _, _ = grid_setup(precision, nx=13, ny=11, nz=9)
+    dt = torch.float32 if precision == "fp32" else torch.float64
+    n = 2 * 4096 + 101
+    g = torch.Generator().manual_seed(7)
+    L = 1.5 * synth.LAMBDA0
+
+    def arr(vals):  # device array starting one element past a 256 B boundary
+        buf = torch.empty(n + 1, dtype=vals.dtype, device="cuda")
+        buf[1:] = vals.cuda()
+        return buf[1:]
+
+    t = {k: arr((torch.rand(n, generator=g, dtype=torch.float64) - 0.5).to(dt) * L)
+         for k in ("x", "y", "z")}
+    t["px"] = arr(torch.arange(n, dtype=dt))                # particle id (exact)
+    for k in ("py", "pz"):
+        t[k] = arr(torch.randn(n, generator=g, dtype=torch.float64).to(dt))
+    t["weight"] = arr(torch.rand(n, generator=g, dtype=torch.float64).to(dt)) if has_w else None
+    t["gamma"] = arr(1 + torch.rand(n, generator=g, dtype=torch.float64).to(dt))
+    types = [synth.ELECTRON, synth.POSITRON, synth.PROTON] if has_type else [synth.ELECTRON]
+    t["type"] = arr(torch.randint(0, 3, (n,), generator=g).to(torch.int16)) if has_type else None
+    ptr = {k: (v.data_ptr() if v is not None else None) for k, v in t.items()}
+    ens = lb.boris_ensemble_wrap_soa(0, lb.BORIS_MEMORY_DEVICE, PREC[precision], n,
+                                     ptr["x"], ptr["y"], ptr["z"], ptr["px"], ptr["py"],
+                                     ptr["pz"], ptr["weight"], ptr["gamma"], ptr["type"], types,
+                                     synth.C_LIGHT)
+    before = {k: v.clone() for k, v in t.items() if v is not None}
+    lb.boris_ensemble_sort_by_cell(ens, h)
+    torch.cuda.synchronize()
+    ids = t["px"].cpu().numpy().astype(np.int64)
+    assert sorted(ids.tolist()) == list(range(n))
+    idc = torch.from_numpy(ids).cuda()
+    for k, v in before.items():
+        assert torch.equal(t[k], v[idc]), k
+    nx, ny = int(params[6]), int(params[7])
+    pos = np.stack([t[k].double().cpu().numpy() for k in ("x", "y", "z")], 1)
+    ci = [np.floor((pos[:, a] - params[a]) / params[3 + a]).astype(np.int64) % int(params[6 + a])
+          for a in range(3)]
+    key = (ci[2] * ny + ci[1]) * nx + ci[0]
+    assert (np.diff(key) >= 0).mean() > 1 - 1e-3
+    same = np.diff(key) == 0
+    assert (np.diff(ids)[same] > 0).mean() > 1 - 1e-3     # stable inside a cell
+    lb.boris_ensemble_destroy(ens)
+    lb.boris_field_destroy(h)
+
+
 def test_sorted_push_equals_unsorted_push_bitwise():
     """The push of each particle is independent of order: sorted and unsorted
     ensembles give bit-identical particles (matched by id)."""
