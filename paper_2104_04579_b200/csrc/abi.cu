@@ -1169,12 +1169,14 @@ static cudaError_t push_deposit_view(boris_ensemble *e, const boris_field *grid,
     const GridArgs<FP> g = make_grid_args<FP>(grid);
     const DepCoefs<FP> dc = make_dep_coefs<FP>(e, grid, dt);
     const EnsView v = e->view();
-    const int64_t ncell = (int64_t)grid->gn[0] * grid->gn[1] * grid->gn[2];
     if (v.layout == BORIS_LAYOUT_SOA) {
-        cudaError_t err = launch_zero3<FP>(Jx, Jy, Jz, ncell, st);
+        DepOut<FP> o;
+        cudaError_t err = dep_scratch_begin<FP>(g, o, st);
         if (err != cudaSuccess) return err;
-        err = launch_push_deposit_soa<FP>(v, g, make_coefs<FP>(e, dt), dc, Jx, Jy, Jz,
-                                          e->multi(), dp, e->device, st);
+        err = launch_push_deposit_soa<FP>(v, g, make_coefs<FP>(e, dt), dc, o, e->multi(), dp,
+                                          e->device, st);
+        if (err == cudaSuccess) return dep_scratch_end<FP>(g, o, Jx, Jy, Jz, st);
+        dep_scratch_free<FP>(o, st);
         if (err != cudaErrorNotSupported) return err;
     }
     // AoS or unaligned: the push, then the deposition (which zeroes J)

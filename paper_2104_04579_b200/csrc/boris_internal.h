@@ -137,14 +137,34 @@ struct DepCoefs {
     FP half_dt;
     DepCoef<FP> t[kMaxTypes];
 };
-// Fused grid-gather push + current deposition (SoA, 16 B-aligned; else
-// cudaErrorNotSupported).  J zeroed by the caller.
+// Deposition target (deposit.cuh): the padded scratch J4, node (i, j, k) for
+// 0 <= i <= nx, 0 <= j <= ny, 0 <= k <= nz with index (k sy + j) sx + i; fp32
+// components interleaved (x, y, z, pad per node), fp64 in three planes.  The +1
+// layers are ghosts that dep_scratch_end folds onto their periodic images.
+template <typename FP>
+struct DepOut {
+    FP *j4;
+    uint32_t sx;     // nx + 1
+    uint32_t sxy;    // (nx + 1)(ny + 1)
+    uint32_t plane;  // (nx + 1)(ny + 1)(nz + 1): fp64 component plane stride
+};
+// Allocates and zeroes J4 for grid g (stream-ordered scratch).
+template <typename FP>
+cudaError_t dep_scratch_begin(const GridArgs<FP> &g, DepOut<FP> &o, cudaStream_t st);
+// Folds J4 into the caller's Jx, Jy, Jz (nx*ny*nz each, overwritten) and frees J4.
+template <typename FP>
+cudaError_t dep_scratch_end(const GridArgs<FP> &g, DepOut<FP> &o, void *Jx, void *Jy, void *Jz,
+                            cudaStream_t st);
+// Frees J4 without folding (error paths).
+template <typename FP>
+void dep_scratch_free(DepOut<FP> &o, cudaStream_t st);
+
+// Fused grid-gather push + current deposition into J4 (SoA, 16 B-aligned; else
+// cudaErrorNotSupported).
 template <typename FP>
 cudaError_t launch_push_deposit_soa(const EnsView &e, const GridArgs<FP> &g, const Coefs<FP> &co,
-                                    const DepCoefs<FP> &dc, void *Jx, void *Jy, void *Jz,
-                                    bool multi, DiagOut *diag, int device, cudaStream_t st);
-template <typename FP>
-cudaError_t launch_zero3(void *Jx, void *Jy, void *Jz, int64_t n, cudaStream_t st);
+                                    const DepCoefs<FP> &dc, const DepOut<FP> &o, bool multi,
+                                    DiagOut *diag, int device, cudaStream_t st);
 
 template <typename FP>
 cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,

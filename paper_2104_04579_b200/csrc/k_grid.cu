@@ -475,16 +475,86 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
 // ---------------------------------------------------------------------------
 // Current deposition (reading c-dep): direct CIC deposition
 // of q w v^{n+1/2} at r^{n+1/2} = r^{n+1} - (dt/2) v^{n+1/2}, divided by the cell
-// volume, with hardware float/double atomics (red.global.add) into J.
+// volume, with hardware atomics (red.global.add) into the padded, interleaved
+// scratch J4 (deposit.cuh), folded into Jx, Jy, Jz at the end.
 // ---------------------------------------------------------------------------
-// Warp-aggregated scatter: lanes holding the same node in CONTIGUOUS lanes (the
-// common case for particles sorted by cell) are summed with a segmented shuffle
-// scan and only each segment's last lane issues the atomics.  Equal nodes in
-// non-contiguous lanes simply stay separate segments (still correct).
+template <typename FP>
+__global__ void k_fold_j4(const DepOut<FP> o, int nx, int ny, int nz, FP *Jx, FP *Jy, FP *Jz) {
+    // component d of node m: fp32 interleaved, fp64 planar
+    constexpr bool kPlanar = sizeof(FP) == 8;
+    const size_t cs = kPlanar ? o.plane : 1, ns = kPlanar ? 1 : 4;
+    const int64_t ncell = (int64_t)nx * ny * nz;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += stride) {
+        const int i = (int)(c % nx);
+        const int j = (int)((c / nx) % ny);
+        const int k = (int)(c / ((int64_t)nx * ny));
+        FP sx_ = FP(0), sy_ = FP(0), sz_ = FP(0);
+        // the node itself and, on the low faces, its ghost images at i + nx etc.
+        for (int cc = 0; cc < (k == 0 ? 2 : 1); ++cc)
+            for (int bb = 0; bb < (j == 0 ? 2 : 1); ++bb)
+                for (int aa = 0; aa < (i == 0 ? 2 : 1); ++aa) {
+                    const FP *p = o.j4 + ns * ((size_t)(k + cc * nz) * o.sxy +
+                                               (size_t)(j + bb * ny) * o.sx + (size_t)(i + aa * nx));
+                    sx_ = b_add(sx_, p[0]);
+                    sy_ = b_add(sy_, p[cs]);
+                    sz_ = b_add(sz_, p[2 * cs]);
+                }
+        Jx[c] = sx_;
+        Jy[c] = sy_;
+        Jz[c] = sz_;
+    }
+}
 
 template <typename FP>
-__device__ __forceinline__ void warp_scatter_add(uint32_t node, FP vx, FP vy, FP vz, FP *Jx,
-                                                 FP *Jy, FP *Jz) {
+cudaError_t dep_scratch_begin(const GridArgs<FP> &g, DepOut<FP> &o, cudaStream_t st) {
+    o.sx = (uint32_t)g.n[0] + 1u;
+    o.sxy = o.sx * ((uint32_t)g.n[1] + 1u);
+    o.plane = o.sxy * ((uint32_t)g.n[2] + 1u);
+    const size_t bytes = (size_t)o.plane * (sizeof(FP) == 4 ? 4 : 3) * sizeof(FP);
+    o.j4 = nullptr;
+    cudaError_t err = scratch_alloc((void **)&o.j4, bytes, st);
+    if (err != cudaSuccess) return err;
+    err = cudaMemsetAsync(o.j4, 0, bytes, st);
+    if (err != cudaSuccess) dep_scratch_free(o, st);
+    return err;
+}
+
+template <typename FP>
+void dep_scratch_free(DepOut<FP> &o, cudaStream_t st) {
+    if (o.j4) scratch_free(o.j4, st);
+    o.j4 = nullptr;
+}
+
+template <typename FP>
+cudaError_t dep_scratch_end(const GridArgs<FP> &g, DepOut<FP> &o, void *Jx, void *Jy, void *Jz,
+                            cudaStream_t st) {
+    const int64_t ncell = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    k_fold_j4<FP><<<grid1d(ncell), 256, 0, st>>>(o, g.n[0], g.n[1], g.n[2], (FP *)Jx, (FP *)Jy,
+                                                 (FP *)Jz);
+    const cudaError_t err = cudaGetLastError();
+    dep_scratch_free(o, st);
+    return err;
+}
+
+template cudaError_t dep_scratch_begin<float>(const GridArgs<float> &, DepOut<float> &,
+                                              cudaStream_t);
+template cudaError_t dep_scratch_begin<double>(const GridArgs<double> &, DepOut<double> &,
+                                               cudaStream_t);
+template cudaError_t dep_scratch_end<float>(const GridArgs<float> &, DepOut<float> &, void *,
+                                            void *, void *, cudaStream_t);
+template cudaError_t dep_scratch_end<double>(const GridArgs<double> &, DepOut<double> &, void *,
+                                             void *, void *, cudaStream_t);
+template void dep_scratch_free<float>(DepOut<float> &, cudaStream_t);
+template void dep_scratch_free<double>(DepOut<double> &, cudaStream_t);
+
+// AoS (any order): one particle per thread; for each corner the lanes holding the
+// same node in CONTIGUOUS lanes (the common case for particles sorted by cell) are
+// summed with a segmented shuffle scan and only each segment's last lane adds the
+// node.  Equal nodes in non-contiguous lanes stay separate segments (still correct).
+template <typename FP>
+__device__ __forceinline__ void warp_scatter_node(const DepOut<FP> &o, uint32_t node, FP vx,
+                                                  FP vy, FP vz) {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const uint32_t prev = __shfl_up_sync(full, node, 1);
@@ -502,17 +572,13 @@ __device__ __forceinline__ void warp_scatter_add(uint32_t node, FP vx, FP vy, FP
             vz = b_add(vz, az);
         }
     }
-    if ((lane == 31 || next != node) && node != kNoNode) {
-        atomicAdd(Jx + node, vx);
-        atomicAdd(Jy + node, vy);
-        atomicAdd(Jz + node, vz);
-    }
+    if ((lane == 31 || next != node) && node != kNoNode) red_node(o, node, vx, vy, vz);
 }
 
 template <typename FP>
 __global__ void __launch_bounds__(256)
-    k_deposit(EnsView e, const __grid_constant__ GridArgs<FP> g,
-              const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz) {
+    k_deposit_aos(EnsView e, const __grid_constant__ GridArgs<FP> g,
+                  const __grid_constant__ DepCoefs<FP> dc, const DepOut<FP> o) {
     constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     // whole blocks iterate together so every lane takes part in the warp shuffles
@@ -522,209 +588,107 @@ __global__ void __launch_bounds__(256)
         FP x = FP(0), y = FP(0), z = FP(0), px = FP(0), py = FP(0), pz = FP(0), w = FP(0);
         int ty = 0;
         if (valid) {
-            if (e.layout == BORIS_LAYOUT_SOA) {
-                x = ((const FP *)e.soa.x)[i];
-                y = ((const FP *)e.soa.y)[i];
-                z = ((const FP *)e.soa.z)[i];
-                px = ((const FP *)e.soa.px)[i];
-                py = ((const FP *)e.soa.py)[i];
-                pz = ((const FP *)e.soa.pz)[i];
-                w = e.soa.w ? ((const FP *)e.soa.w)[i] : FP(1);
-                if (e.soa.type) ty = e.soa.type[i];
-            } else {
-                const FP *r = (const FP *)((const unsigned char *)e.aos + i * RB);
-                x = r[0]; y = r[1]; z = r[2];
-                px = r[3]; py = r[4]; pz = r[5];
-                w = r[6];
-                ty = *(const int16_t *)(r + 8);
-            }
+            const FP *r = (const FP *)((const unsigned char *)e.aos + i * RB);
+            x = r[0]; y = r[1]; z = r[2];
+            px = r[3]; py = r[4]; pz = r[5];
+            w = r[6];
+            ty = *(const int16_t *)(r + 8);
         }
-        const DepCoef<FP> t = dc.t[dc.n_types > 1 ? ty : 0];
-        const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
-        // v = p/(gamma m) = u/(S m gamma)
-        const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
-        const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
-        // half-step position
-        const FP xh = b_fma(-dc.half_dt, vx, x), yh = b_fma(-dc.half_dt, vy, y),
-                 zh = b_fma(-dc.half_dt, vz, z);
-        int ix[2], iy[2], iz[2];
-        FP fx, fy, fz;
-        grid_axis<FP>(xh, g.org[0], g.inv_h[0], g.nf[0], g.inv_nf[0], g.n[0], ix[0], ix[1], fx);
-        grid_axis<FP>(yh, g.org[1], g.inv_h[1], g.nf[1], g.inv_nf[1], g.n[1], iy[0], iy[1], fy);
-        grid_axis<FP>(zh, g.org[2], g.inv_h[2], g.nf[2], g.inv_nf[2], g.n[2], iz[0], iz[1], fz);
-        const FP wx[2] = {b_add(FP(1), -fx), fx};
-        const FP wy[2] = {b_add(FP(1), -fy), fy};
-        const FP wz[2] = {b_add(FP(1), -fz), fz};
-        const FP qw = b_mul(t.q_vol, w);
+        typename WarpRun<FP>::Part p;
+        WarpRun<FP>::prepare(g, dc.t[dc.n_types > 1 ? ty : 0], dc.half_dt, x, y, z, px, py, pz,
+                             w, p);
+        const uint32_t nb = valid ? base_node(g, o, p.l) : kNoNode;
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int b = 0; b < 2; ++b) {
-                const FP wyz = b_mul(qw, b_mul(wy[b], wz[c]));
-                const uint32_t row =
-                    ((uint32_t)iz[c] * (uint32_t)g.n[1] + (uint32_t)iy[b]) * (uint32_t)g.n[0];
-#pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                    const FP s = b_mul(wx[a], wyz);
-                    const uint32_t node = valid ? row + (uint32_t)ix[a] : kNoNode;
-                    warp_scatter_add<FP>(node, b_mul(s, vx), b_mul(s, vy), b_mul(s, vz), Jx, Jy,
-                                         Jz);
-                }
-            }
+        for (int q = 0; q < 8; ++q)
+            warp_scatter_node<FP>(o, valid ? nb + corner(o, q) : kNoNode, b_mul(p.sw[q], p.qv[0]),
+                                  b_mul(p.sw[q], p.qv[1]), b_mul(p.sw[q], p.qv[2]));
     }
 }
 
 // ---------------------------------------------------------------------------
-// Run-accumulating deposition (SoA): each lane deposits K consecutive particles,
-// keeping the 8 nodes x 3 components of its current cell in registers and
-// issuing atomics only when the cell changes.  For particles sorted by cell
-// (boris_ensemble_sort_by_cell) one flush covers a whole run.  Warp tiles are
-// staged through shared memory with coalesced loads and a skewed layout
-// (p -> p + p/K) so the per-lane sequential reads are bank-conflict free.
+// Lane-run deposition (fp32 SoA, 16 B-aligned arrays): each lane deposits K = 8
+// consecutive particles, loaded with two 128-bit loads per array (a warp's loads
+// cover its 256-particle tile contiguously), keeping the 8 nodes x 3 components
+// of its current cell in registers and issuing atomics only when the cell
+// changes.  For particles sorted by cell (boris_ensemble_sort_by_cell) one flush
+// covers a whole run; at the end of a tile the lanes' open cells are merged.
 // ---------------------------------------------------------------------------
-template <typename FP>
-struct DepRuns {
-    static constexpr int K = 8;          // particles per lane per tile
-    static constexpr int WARPS = sizeof(FP) == 4 ? 4 : 2;  // <= 48 KB static smem
-    static constexpr int TILE = 32 * K;  // particles per warp tile
-    static constexpr int SK = TILE + TILE / K;
-};
+constexpr int kDepK = 8;            // particles per lane per tile
+constexpr int kDepWarps = 8;        // warps per block
+constexpr int kDepTile = 32 * kDepK;
 
-// fp32 with 16 B-aligned arrays: DIRECT (no shared-memory staging; each lane
-// loads its K = 8 consecutive particles with two 128-bit loads per array, a
-// warp's loads cover the tile contiguously).  fp64 or unaligned: staged tiles.
-#ifndef BORIS_DEP_PREFETCH
-#define BORIS_DEP_PREFETCH 0
-#endif
 #ifndef BORIS_DEP_DIRECT_MINB
-#define BORIS_DEP_DIRECT_MINB (BORIS_DEP_PREFETCH ? 1 : 2)
+#define BORIS_DEP_DIRECT_MINB 2
 #endif
-template <typename FP, bool DIRECT>
-__global__ void __launch_bounds__((DIRECT ? 8 : DepRuns<FP>::WARPS) * 32,
-                                  DIRECT ? BORIS_DEP_DIRECT_MINB : 6)
-    k_deposit_runs(EnsView e, const __grid_constant__ GridArgs<FP> g,
-                   const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz) {
-    using R = DepRuns<FP>;
-    constexpr int NW = DIRECT ? 8 : R::WARPS;
-    __shared__ FP s[DIRECT ? 1 : R::WARPS][7][DIRECT ? 1 : R::SK];
-    __shared__ int16_t s_ty[DIRECT ? 1 : R::WARPS][DIRECT ? 1 : R::SK];
-    __shared__ typename DepositRun<FP>::MergeSmem s_merge[DIRECT && kTransposedMerge<FP> ? 8 : 1];
+__global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
+    k_deposit_runs(EnsView e, const __grid_constant__ GridArgs<float> g,
+                   const __grid_constant__ DepCoefs<float> dc, const DepOut<float> o) {
+    __shared__ DepositRun<float>::MergeSmem s_merge[kTransposedMerge<float> ? kDepWarps : 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const FP *arr[7] = {(const FP *)e.soa.x, (const FP *)e.soa.y, (const FP *)e.soa.z,
-                        (const FP *)e.soa.px, (const FP *)e.soa.py, (const FP *)e.soa.pz,
-                        (const FP *)e.soa.w};
+    const float *arr[7] = {(const float *)e.soa.x, (const float *)e.soa.y, (const float *)e.soa.z,
+                           (const float *)e.soa.px, (const float *)e.soa.py,
+                           (const float *)e.soa.pz, (const float *)e.soa.w};
     const bool multi = dc.n_types > 1 && e.soa.type;
-    const int64_t stride = (int64_t)gridDim.x * NW * R::TILE;
-    FP rv[DIRECT ? 7 : 1][DIRECT ? R::K : 1];
-    int16_t rty[DIRECT ? R::K : 1];
-    // DIRECT: lane's K = 8 consecutive particles of the tile at `tb`, two 128-bit
-    // loads per array (scalar loads in the ragged last tile).
-    auto load_direct = [&](int64_t tb, FP (&dv)[DIRECT ? 7 : 1][DIRECT ? R::K : 1],
-                           int16_t (&dty)[DIRECT ? R::K : 1]) {
-        if constexpr (DIRECT) {
-            static_assert(sizeof(FP) == 4 && R::K == 8, "direct staging: fp32, K = 8");
-            const int64_t i0 = tb + lane * R::K;
-            if (i0 + R::K <= e.n) {
-#pragma unroll
-                for (int a = 0; a < 7; ++a)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        float4 v = arr[a] ? __ldg(reinterpret_cast<const float4 *>(arr[a] + i0) + h)
-                                          : make_float4(1.f, 1.f, 1.f, 1.f);
-                        dv[a][4 * h] = v.x; dv[a][4 * h + 1] = v.y;
-                        dv[a][4 * h + 2] = v.z; dv[a][4 * h + 3] = v.w;
-                    }
-                if (multi) {
-                    const uint4 t4 = __ldg(reinterpret_cast<const uint4 *>(e.soa.type + i0));
-                    const uint32_t tw[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-                    for (int j = 0; j < R::K; ++j)
-                        dty[j] = (int16_t)(tw[j >> 1] >> (16 * (j & 1)));
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < R::K; ++j) {
-                    const int64_t i = i0 + j;
-#pragma unroll
-                    for (int a = 0; a < 7; ++a)
-                        dv[a][j] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
-                    dty[j] = (multi && i < e.n) ? e.soa.type[i] : (int16_t)0;
-                }
-            }
-        }
-    };
-#if BORIS_DEP_PREFETCH
-    // software pipeline: the next tile's loads are in flight during this tile's
-    // arithmetic, scan and atomics
-    FP nv[DIRECT ? 7 : 1][DIRECT ? R::K : 1];
-    int16_t nty[DIRECT ? R::K : 1];
-    const int64_t first = ((int64_t)blockIdx.x * NW + warp) * R::TILE;
-    if (DIRECT && first < e.n) load_direct(first, nv, nty);
-#endif
-    for (int64_t base = ((int64_t)blockIdx.x * NW + warp) * R::TILE; base < e.n;
+    const int64_t stride = (int64_t)gridDim.x * kDepWarps * kDepTile;
+    for (int64_t base = ((int64_t)blockIdx.x * kDepWarps + warp) * kDepTile; base < e.n;
          base += stride) {
-        if constexpr (DIRECT) {
-#if BORIS_DEP_PREFETCH
+        // lane's K = 8 consecutive particles: two 128-bit loads per array (scalar
+        // loads in the ragged last tile)
+        float rv[7][kDepK];
+        int16_t rty[kDepK];
+        const int64_t i0 = base + lane * kDepK;
+        if (i0 + kDepK <= e.n) {
 #pragma unroll
-            for (int j = 0; j < R::K; ++j) {
+            for (int a = 0; a < 7; ++a)
 #pragma unroll
-                for (int a = 0; a < 7; ++a) rv[a][j] = nv[a][j];
-                rty[j] = nty[j];
+                for (int h = 0; h < 2; ++h) {
+                    const float4 v = arr[a] ? __ldg(reinterpret_cast<const float4 *>(arr[a] + i0) + h)
+                                            : make_float4(1.f, 1.f, 1.f, 1.f);
+                    rv[a][4 * h] = v.x; rv[a][4 * h + 1] = v.y;
+                    rv[a][4 * h + 2] = v.z; rv[a][4 * h + 3] = v.w;
+                }
+            if (multi) {
+                const uint4 t4 = __ldg(reinterpret_cast<const uint4 *>(e.soa.type + i0));
+                const uint32_t tw[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                for (int j = 0; j < kDepK; ++j) rty[j] = (int16_t)(tw[j >> 1] >> (16 * (j & 1)));
             }
-            if (base + stride < e.n) load_direct(base + stride, nv, nty);
-#else
-            load_direct(base, rv, rty);
-#endif
         } else {
-            // coalesced warp loads into the skewed tile
 #pragma unroll
-            for (int r = 0; r < R::K; ++r) {
-                const int p = r * 32 + lane;
-                const int64_t i = base + p;
-                const int sp = p + p / R::K;
+            for (int j = 0; j < kDepK; ++j) {
+                const int64_t i = i0 + j;
 #pragma unroll
                 for (int a = 0; a < 7; ++a)
-                    s[warp][a][sp] = (i < e.n) ? (arr[a] ? arr[a][i] : FP(1)) : FP(0);
-                if (multi) s_ty[warp][sp] = (i < e.n) ? e.soa.type[i] : (int16_t)0;
+                    rv[a][j] = (i < e.n) ? (arr[a] ? arr[a][i] : 1.f) : 0.f;
+                rty[j] = (multi && i < e.n) ? e.soa.type[i] : (int16_t)0;
             }
-            __syncwarp();
         }
-        DepositRun<FP> run;
+        DepositRun<float> run;
         run.reset();
-        constexpr int kUnrollJ = DIRECT ? R::K : 1;  // register arrays need constant indices
-#pragma unroll kUnrollJ
-        for (int j = 0; j < R::K; ++j) {
-            const int p = lane * R::K + j;
-            if (base + p >= e.n) break;
-            const int sp = DIRECT ? 0 : p + p / R::K;
-            const FP x = DIRECT ? rv[0][j] : s[warp][0][sp];
-            const FP y = DIRECT ? rv[1][j] : s[warp][1][sp];
-            const FP z = DIRECT ? rv[2][j] : s[warp][2][sp];
-            const FP px = DIRECT ? rv[3][j] : s[warp][3][sp];
-            const FP py = DIRECT ? rv[4][j] : s[warp][4][sp];
-            const FP pz = DIRECT ? rv[5][j] : s[warp][5][sp];
-            const FP w = DIRECT ? rv[6][j] : s[warp][6][sp];
-            const DepCoef<FP> t = dc.t[multi ? (DIRECT ? rty[j] : s_ty[warp][sp]) : 0];
-            run.add(g, t, dc.half_dt, x, y, z, px, py, pz, w, Jx, Jy, Jz);
+#pragma unroll
+        for (int j = 0; j < kDepK; ++j) {
+            if (i0 + j >= e.n) break;
+            run.add(g, o, dc.t[multi ? rty[j] : 0], dc.half_dt, rv[0][j], rv[1][j], rv[2][j],
+                    rv[3][j], rv[4][j], rv[5][j], rv[6][j]);
         }
-        // end of tile: merge lanes holding the same cell, one atomic per segment
-        if constexpr (DIRECT && kTransposedMerge<FP>) {
-            run.merge_flush(g, Jx, Jy, Jz, s_merge[warp], lane);
+        // end of tile: merge lanes holding the same cell, one atomic set per run
+        if constexpr (kTransposedMerge<float>) {
+            run.merge_flush(o, s_merge[warp], lane);
         } else {
-            run.warp_merge(g, lane);
-            run.flush(g, Jx, Jy, Jz);
+            run.warp_merge(lane);
+            run.flush(o);
         }
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------
-// Warp-run deposition (SoA, any alignment; deposit.cuh WarpRun): each warp owns a
-// contiguous chunk of particles and walks it in rounds of 32 consecutive
-// particles (lane l takes particle base + l: 4/8 B loads, warp-coalesced), PD
-// rounds of loads in flight ahead of the arithmetic (register ring).  Sorted by
-// cell, a round almost always lies in the warp's open cell: 24 FMA per particle,
-// one warp reduction + one 24-lane atomic instruction per cell.
+// Warp-run deposition (fp64, or fp32 with unaligned arrays; deposit.cuh WarpRun):
+// each warp owns a contiguous chunk of particles and walks it in rounds of 32
+// consecutive particles (lane l takes particle base + l: 4/8 B loads,
+// warp-coalesced), PD rounds of loads in flight ahead of the arithmetic (register
+// ring).  Sorted by cell, a round almost always lies in the warp's open cell: 24
+// FMA per particle, one warp reduction + 8 node atomics per cell.
 // ---------------------------------------------------------------------------
 #ifndef BORIS_DW_PD
 #define BORIS_DW_PD 3
@@ -742,8 +706,7 @@ struct DepWarp {
 template <typename FP, bool MULTI>
 __global__ void __launch_bounds__(DepWarp<FP>::WARPS * 32, DepWarp<FP>::MINB)
     k_deposit_warp(EnsView e, const __grid_constant__ GridArgs<FP> g,
-                   const __grid_constant__ DepCoefs<FP> dc, FP *Jx, FP *Jy, FP *Jz,
-                   int64_t chunk) {
+                   const __grid_constant__ DepCoefs<FP> dc, const DepOut<FP> o, int64_t chunk) {
     using D = DepWarp<FP>;
     constexpr int PD = D::PD;
     __shared__ WarpRunSmem<FP> sm[D::WARPS];
@@ -782,77 +745,63 @@ __global__ void __launch_bounds__(DepWarp<FP>::WARPS * 32, DepWarp<FP>::MINB)
             typename WarpRun<FP>::Part part;
             WarpRun<FP>::prepare(g, dc.t[MULTI ? t : 0], dc.half_dt, v[0], v[1], v[2], v[3],
                                  v[4], v[5], v[6], part);
-            run.round(g, part, i < end, Jx, Jy, Jz, sm[warp], lane);
+            run.round(g, o, part, i < end, sm[warp], lane);
         }
     }
-    if (run.open) run.flush(g, Jx, Jy, Jz, sm[warp], lane);
+    if (run.open) run.flush(g, o, sm[warp], lane);
 }
 
 template <typename FP>
-__global__ void k_zero3(FP *a, FP *b, FP *c, int64_t n) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        a[i] = FP(0);
-        b[i] = FP(0);
-        c[i] = FP(0);
+static cudaError_t launch_deposit_kernel(const EnsView &e, const GridArgs<FP> &g,
+                                         const DepCoefs<FP> &dc, const DepOut<FP> &o, int device,
+                                         cudaStream_t st) {
+    if (e.n == 0) return cudaSuccess;
+    if (e.layout == BORIS_LAYOUT_AOS) {
+        const int64_t blocks = (e.n + 255) / 256;
+        const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
+        k_deposit_aos<FP><<<grid, 256, 0, st>>>(e, g, dc, o);
+        return cudaGetLastError();
     }
-}
-
-// Zero J: one launch for the three arrays (three memsets cost ~3 launch gaps).
-template <typename FP>
-cudaError_t launch_zero3(void *Jx, void *Jy, void *Jz, int64_t n, cudaStream_t st) {
-    const int64_t blocks = (n + 255) / 256;
-    k_zero3<FP><<<(unsigned)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, st>>>(
-        (FP *)Jx, (FP *)Jy, (FP *)Jz, n);
+    // fp32 with 16 B-aligned arrays: lane runs (128-bit loads); fp64 or unaligned:
+    // warp runs.  Measured on 10^7 sorted particles, 64^3 grid: fp32 11.0 (lane) vs
+    // 13.2 ps (warp), fp64 34.0 (lane, staged tiles) vs 22.5 ps (warp).
+    if constexpr (sizeof(FP) == 4) {
+        auto al16 = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
+        if (al16(e.soa.x) && al16(e.soa.y) && al16(e.soa.z) && al16(e.soa.px) &&
+            al16(e.soa.py) && al16(e.soa.pz) && al16(e.soa.w) && al16(e.soa.type)) {
+            const int64_t tiles = (e.n + kDepTile - 1) / kDepTile;
+            const int64_t blocks = (tiles + kDepWarps - 1) / kDepWarps;
+            const unsigned grid = (unsigned)stream_grid(blocks, 4, device);
+            k_deposit_runs<<<grid, kDepWarps * 32, 0, st>>>(e, g, dc, o);
+            return cudaGetLastError();
+        }
+    }
+    // one contiguous chunk per warp, a multiple of 32 particles, sized so the
+    // resident blocks cover the ensemble in one wave
+    using D = DepWarp<FP>;
+    const int64_t warps = (int64_t)sm_count(device) * D::MINB * D::WARPS;
+    int64_t chunk = (e.n + warps - 1) / warps;
+    chunk = (chunk + 31) / 32 * 32;
+    const int64_t blocks = ((e.n + chunk - 1) / chunk + D::WARPS - 1) / D::WARPS;
+    if (dc.n_types > 1 && e.soa.type)
+        k_deposit_warp<FP, true><<<(unsigned)blocks, D::WARPS * 32, 0, st>>>(e, g, dc, o, chunk);
+    else
+        k_deposit_warp<FP, false><<<(unsigned)blocks, D::WARPS * 32, 0, st>>>(e, g, dc, o, chunk);
     return cudaGetLastError();
 }
-template cudaError_t launch_zero3<float>(void *, void *, void *, int64_t, cudaStream_t);
-template cudaError_t launch_zero3<double>(void *, void *, void *, int64_t, cudaStream_t);
 
 template <typename FP>
 cudaError_t launch_deposit(const EnsView &e, const GridArgs<FP> &g, const DepCoefs<FP> &dc,
                            void *Jx, void *Jy, void *Jz, int device, cudaStream_t st) {
-    const int64_t ncell = (int64_t)g.n[0] * g.n[1] * g.n[2];
-    cudaError_t err = launch_zero3<FP>(Jx, Jy, Jz, ncell, st);
-    if (err != cudaSuccess || e.n == 0) return err;
-    // fp32 with 16 B-aligned arrays: lane runs (k_deposit_runs DIRECT, 128-bit loads);
-    // fp64 or unaligned: warp runs (k_deposit_warp).  Measured on 10^7 sorted
-    // particles, 64^3 grid: fp32 11.0 (lane) vs 13.2 ps (warp), fp64 34.0 vs 22.5 ps.
-    if constexpr (sizeof(FP) == 4) {
-        auto al16 = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
-        if (e.layout == BORIS_LAYOUT_SOA && al16(e.soa.x) && al16(e.soa.y) && al16(e.soa.z) &&
-            al16(e.soa.px) && al16(e.soa.py) && al16(e.soa.pz) && al16(e.soa.w) &&
-            al16(e.soa.type)) {
-            using R = DepRuns<FP>;
-            const int64_t tiles = (e.n + R::TILE - 1) / R::TILE;
-            const int64_t blocks = (tiles + 7) / 8;
-            const unsigned grid = (unsigned)stream_grid(blocks, 4, device);
-            k_deposit_runs<FP, true><<<grid, 8 * 32, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy,
-                                                               (FP *)Jz);
-            return cudaGetLastError();
-        }
+    DepOut<FP> o;
+    cudaError_t err = dep_scratch_begin<FP>(g, o, st);
+    if (err != cudaSuccess) return err;
+    err = launch_deposit_kernel<FP>(e, g, dc, o, device, st);
+    if (err != cudaSuccess) {
+        dep_scratch_free<FP>(o, st);
+        return err;
     }
-    if (e.layout == BORIS_LAYOUT_SOA) {
-        // one contiguous chunk per warp, a multiple of 32 particles, sized so the
-        // resident blocks cover the ensemble in one wave
-        using D = DepWarp<FP>;
-        const int64_t warps = (int64_t)sm_count(device) * D::MINB * D::WARPS;
-        int64_t chunk = (e.n + warps - 1) / warps;
-        chunk = (chunk + 31) / 32 * 32;
-        const int64_t blocks = ((e.n + chunk - 1) / chunk + D::WARPS - 1) / D::WARPS;
-        const bool multi = dc.n_types > 1 && e.soa.type;
-        if (multi)
-            k_deposit_warp<FP, true><<<(unsigned)blocks, D::WARPS * 32, 0, st>>>(
-                e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz, chunk);
-        else
-            k_deposit_warp<FP, false><<<(unsigned)blocks, D::WARPS * 32, 0, st>>>(
-                e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz, chunk);
-        return cudaGetLastError();
-    }
-    const int64_t blocks = (e.n + 255) / 256;
-    const unsigned grid = (unsigned)stream_grid(blocks, 8, device);
-    k_deposit<FP><<<grid, 256, 0, st>>>(e, g, dc, (FP *)Jx, (FP *)Jy, (FP *)Jz);
-    return cudaGetLastError();
+    return dep_scratch_end<FP>(g, o, Jx, Jy, Jz, st);
 }
 
 template cudaError_t launch_deposit<float>(const EnsView &, const GridArgs<float> &,

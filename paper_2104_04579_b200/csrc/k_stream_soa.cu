@@ -286,7 +286,7 @@ template <typename FP, bool MULTI, bool DIAG>
 __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
     k_push_deposit_soa(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
                        const __grid_constant__ Coefs<FP> co, const __grid_constant__ DepCoefs<FP> dc,
-                       FP *Jx, FP *Jy, FP *Jz, int64_t n_groups, int64_t n, double *partials) {
+                       const DepOut<FP> o, int64_t n_groups, int64_t n, double *partials) {
     constexpr int V = Vec<FP>::N;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     __shared__ DepCoef<FP> s_d[MULTI ? kMaxTypes : 1];
@@ -351,14 +351,14 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             // stored p after the stores beats carrying the push's u and 1/gamma)
 #pragma unroll
             for (int j = 0; j < V; ++j)
-                run.add(g, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j], y.v[j], z.v[j],
-                        px.v[j], py.v[j], pz.v[j], w.v[j], Jx, Jy, Jz);
+                run.add(g, o, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j], y.v[j], z.v[j],
+                        px.v[j], py.v[j], pz.v[j], w.v[j]);
         }
         if constexpr (kTransposedMergePD<FP>) {
-            run.merge_flush(g, Jx, Jy, Jz, s_merge[threadIdx.x >> 5], lane);
+            run.merge_flush(o, s_merge[threadIdx.x >> 5], lane);
         } else {
-            run.warp_merge(g, lane);
-            run.flush(g, Jx, Jy, Jz);
+            run.warp_merge(lane);
+            run.flush(o);
         }
     }
     // ragged tail (n mod V particles): push then deposit directly
@@ -379,34 +379,34 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
         }
         DepositRun<FP> run;
         run.reset();
-        run.add(g, MULTI ? s_d[ty] : dc.t[0], dc.half_dt, x, y, z, px, py, pz, w, Jx, Jy, Jz);
-        run.flush(g, Jx, Jy, Jz);
+        run.add(g, o, MULTI ? s_d[ty] : dc.t[0], dc.half_dt, x, y, z, px, py, pz, w);
+        run.flush(o);
     }
     if (DIAG) block_diag_partial<kStreamThreads>(ke, cnt, partials);
 }
 
 template <typename FP, bool MULTI, bool DIAG>
 static cudaError_t dispatch_push_deposit(const EnsView &e, const GridArgs<FP> &g,
-                                         const Coefs<FP> &co, const DepCoefs<FP> &dc, FP *J[3],
-                                         DiagOut *diag, int device, cudaStream_t st) {
+                                         const Coefs<FP> &co, const DepCoefs<FP> &dc,
+                                         const DepOut<FP> &o, DiagOut *diag, int device,
+                                         cudaStream_t st) {
     constexpr int V = Vec<FP>::N;
     const int64_t n_groups = e.n / V;
     const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, BORIS_PD_MINB, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
     k_push_deposit_soa<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
-        e.soa, g, co, dc, J[0], J[1], J[2], n_groups, e.n, diag ? diag->partials : nullptr);
+        e.soa, g, co, dc, o, n_groups, e.n, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }
 
 // Returns cudaErrorNotSupported when the state arrays are not 16 B aligned (the
-// caller then runs the push and the deposition as two launches).  J is zeroed
-// by the caller.
+// caller then runs the push and the deposition as two launches).
 template <typename FP>
 cudaError_t launch_push_deposit_soa(const EnsView &e, const GridArgs<FP> &g, const Coefs<FP> &co,
-                                    const DepCoefs<FP> &dc, void *Jx, void *Jy, void *Jz,
-                                    bool multi, DiagOut *diag, int device, cudaStream_t st) {
+                                    const DepCoefs<FP> &dc, const DepOut<FP> &o, bool multi,
+                                    DiagOut *diag, int device, cudaStream_t st) {
     constexpr int V = Vec<FP>::N;
     if (e.n == 0) {
         if (diag) diag->written = 0;
@@ -417,23 +417,23 @@ cudaError_t launch_push_deposit_soa(const EnsView &e, const GridArgs<FP> &g, con
                     aligned16(e.soa.g) && (!e.soa.w || aligned16(e.soa.w)) &&
                     (!multi || ((uintptr_t)e.soa.type & (2 * V - 1)) == 0);
     if (!al) return cudaErrorNotSupported;
-    FP *J[3] = {(FP *)Jx, (FP *)Jy, (FP *)Jz};
     const bool d = diag != nullptr;
     if (multi)
-        return d ? dispatch_push_deposit<FP, true, true>(e, g, co, dc, J, diag, device, st)
-                 : dispatch_push_deposit<FP, true, false>(e, g, co, dc, J, diag, device, st);
-    return d ? dispatch_push_deposit<FP, false, true>(e, g, co, dc, J, diag, device, st)
-             : dispatch_push_deposit<FP, false, false>(e, g, co, dc, J, diag, device, st);
+        return d ? dispatch_push_deposit<FP, true, true>(e, g, co, dc, o, diag, device, st)
+                 : dispatch_push_deposit<FP, true, false>(e, g, co, dc, o, diag, device, st);
+    return d ? dispatch_push_deposit<FP, false, true>(e, g, co, dc, o, diag, device, st)
+             : dispatch_push_deposit<FP, false, false>(e, g, co, dc, o, diag, device, st);
 }
 
 template cudaError_t launch_push_deposit_soa<float>(const EnsView &, const GridArgs<float> &,
                                                     const Coefs<float> &, const DepCoefs<float> &,
-                                                    void *, void *, void *, bool, DiagOut *, int,
+                                                    const DepOut<float> &, bool, DiagOut *, int,
                                                     cudaStream_t);
 template cudaError_t launch_push_deposit_soa<double>(const EnsView &, const GridArgs<double> &,
                                                      const Coefs<double> &,
-                                                     const DepCoefs<double> &, void *, void *,
-                                                     void *, bool, DiagOut *, int, cudaStream_t);
+                                                     const DepCoefs<double> &,
+                                                     const DepOut<double> &, bool, DiagOut *, int,
+                                                     cudaStream_t);
 
 // Unaligned inputs (e.g. sliced torch tensors): one particle per thread, scalar
 // accesses, the same push_one arithmetic.
