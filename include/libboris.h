@@ -73,7 +73,7 @@ typedef struct boris_particle_type {
     double charge;
     double mass;
 } boris_particle_type;
-#define BORIS_MAX_TYPES 32
+#define BORIS_MAX_TYPES 256
 
 /* Largest particle count of one ensemble handle (2^40). */
 #define BORIS_MAX_PARTICLES ((int64_t)1 << 40)

@@ -35,7 +35,7 @@ BORIS_FP32 = 0
 BORIS_FP64 = 1
 BORIS_MEMORY_DEVICE = 0
 BORIS_MEMORY_HOST = 1
-BORIS_MAX_TYPES = 32
+BORIS_MAX_TYPES = 256
 BORIS_MAX_PARTICLES = 1 << 40
 BORIS_PUSH_AUTO = 0
 BORIS_PUSH_STREAM_EACH_STEP = 1

@@ -24,9 +24,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "libboris.h"
+
 namespace boris {
 
-constexpr int kMaxTypes = 32;  // == BORIS_MAX_TYPES
+#ifndef BORIS_KMAX_TYPES
+#define BORIS_KMAX_TYPES BORIS_MAX_TYPES
+#endif
+constexpr int kMaxTypes = BORIS_KMAX_TYPES;  // == BORIS_MAX_TYPES (tuning builds may shrink it)
 
 // Per-type coefficients, computed in double on the host for each push and
 // cast to FP.
@@ -45,11 +50,30 @@ struct TypeCoef {
 // Momentum update scheme (readings c-vay, c-hc in DESIGN.md).
 enum Pusher { PUSHER_BORIS = 0, PUSHER_VAY = 1, PUSHER_HIGUERA_CARY = 2 };
 
-template <typename FP>
-struct Coefs {
+template <typename FP, int NT>
+struct CoefsN {
     int n_types;  // table entries used
-    TypeCoef<FP> t[kMaxTypes];
+    TypeCoef<FP> t[NT];
 };
+// The full per-push table (host side, multi-type kernels).
+template <typename FP>
+using Coefs = CoefsN<FP, kMaxTypes>;
+// A kernel instantiation's parameter block: single-type kernels read t[0] only, so
+// they take a one-entry table (a 256-entry fp32 table in every launch's parameter
+// block measured +0.4-1.0 us per push on 4096-particle launches).
+template <typename FP, bool MULTI>
+using KCoefs = CoefsN<FP, MULTI ? kMaxTypes : 1>;
+template <bool MULTI, typename FP>
+inline KCoefs<FP, MULTI> kcoefs(const Coefs<FP> &co) {
+    if constexpr (MULTI) {
+        return co;
+    } else {
+        KCoefs<FP, false> k;
+        k.n_types = co.n_types;
+        k.t[0] = co.t[0];
+        return k;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Correctly rounded elementary operations (IEEE round-to-nearest, reading c14),
@@ -546,8 +570,8 @@ __device__ __forceinline__ void block_diag_partial(double ke, double count, doub
 
 // Load the type table into shared memory (multi-type kernels).  Divergent
 // indexing into the kernel-parameter bank serialises; shared memory does not.
-template <typename FP>
-__device__ __forceinline__ void load_type_table(const Coefs<FP> &co, TypeCoef<FP> *s_t) {
+template <typename FP, int NT>
+__device__ __forceinline__ void load_type_table(const CoefsN<FP, NT> &co, TypeCoef<FP> *s_t) {
     for (int i = threadIdx.x; i < co.n_types; i += blockDim.x) s_t[i] = co.t[i];
     __syncthreads();
 }

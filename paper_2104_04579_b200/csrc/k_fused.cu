@@ -395,7 +395,7 @@ constexpr int kTimeTab = 1024;
 template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER, bool YZ>
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
-            const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
+            const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_steps, double *partials) {
     constexpr int kFlush = kFlushOf<FP>;
     constexpr bool kMerged = kMergedRsqrt<FP, FIELD>;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
@@ -619,7 +619,7 @@ static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
                                         : &k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, false>;
     int64_t grid = fused_grid((const void *)kern, blocks > 0 ? blocks : 1, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, co, n_steps,
+    kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, kcoefs<MULTI>(co), n_steps,
                                                   diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();

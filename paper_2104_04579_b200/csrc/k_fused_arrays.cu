@@ -15,7 +15,8 @@ namespace boris {
 template <typename FP, int LAYOUT, bool MULTI, bool DIAG, int PUSHER>
 __global__ void __launch_bounds__(kFusedThreads)
     k_fused_arrays(EnsView e, FieldSoaPtrs f, const void *frec,
-                   const __grid_constant__ Coefs<FP> co, int64_t n_steps, double *partials) {
+                   const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_steps,
+                   double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     if (MULTI) load_type_table(co, s_t);
     double ke = 0.0, cnt = 0.0;
@@ -85,7 +86,7 @@ static cudaError_t dispatch_fa(const EnsView &e, const FieldSoaPtrs &f, const vo
     int64_t grid = fused_grid((const void *)kern, blocks > 0 ? blocks : 1, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
     kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(
-        e, f, frec, co, n_steps, diag ? diag->partials : nullptr);
+        e, f, frec, kcoefs<MULTI>(co), n_steps, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }

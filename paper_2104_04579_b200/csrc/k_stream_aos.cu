@@ -37,7 +37,8 @@ struct AosGeom {
 // Push particle j of a shared-memory record tile (record layout of libboris.h).
 template <typename FP, bool MULTI, bool DIAG>
 __device__ __forceinline__ void push_record(unsigned char *rec, const FP *fld,
-                                            const Coefs<FP> &co, const TypeCoef<FP> *s_t, double &ke,
+                                            const KCoefs<FP, MULTI> &co, const TypeCoef<FP> *s_t,
+                                            double &ke,
                                             double &cnt) {
     FP *r = (FP *)rec;
     const int ty = MULTI ? *(const int16_t *)(rec + AosGeom<FP>::TYPE_OFF) : 0;
@@ -57,7 +58,7 @@ __device__ __forceinline__ void push_record(unsigned char *rec, const FP *fld,
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void __launch_bounds__(kAosThreads)
     k_stream_aos(unsigned char *rec, const unsigned char *frec,
-                 const __grid_constant__ Coefs<FP> co, int64_t n_tiles, int64_t n_main,
+                 const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_tiles, int64_t n_main,
                  int64_t n, double *partials) {
     using Gm = AosGeom<FP>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -148,7 +149,7 @@ static cudaError_t dispatch_aos(const EnsView &e, const void *frec, const Coefs<
     if (grid > n_tiles) grid = n_tiles > 0 ? n_tiles : 1;
     if (DIAG && grid > diag->cap) grid = diag->cap;
     kern<<<(unsigned)grid, kAosThreads, Gm::SMEM, st>>>(
-        (unsigned char *)e.aos, (const unsigned char *)frec, co, n_tiles, n_main, e.n,
+        (unsigned char *)e.aos, (const unsigned char *)frec, kcoefs<MULTI>(co), n_tiles, n_main, e.n,
         diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();

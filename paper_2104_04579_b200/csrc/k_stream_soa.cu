@@ -21,7 +21,7 @@ namespace boris {
 
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
-    k_stream_soa_vec(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ Coefs<FP> co,
+    k_stream_soa_vec(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ KCoefs<FP, MULTI> co,
                      int64_t n_groups, int64_t n, double *partials) {
     constexpr int V = Vec<FP>::N;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void BORIS_GRID_BOUNDS
     k_stream_soa_grid(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
-                      const __grid_constant__ Coefs<FP> co, int64_t n_groups, int64_t n,
+                      const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_groups, int64_t n,
                       double *partials) {
     constexpr int V = Vec<FP>::N;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
@@ -234,7 +234,7 @@ static cudaError_t dispatch_soa_grid(const EnsView &e, const GridArgs<FP> &g,
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
     k_stream_soa_grid<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
-        e.soa, g, co, n_groups, e.n, diag ? diag->partials : nullptr);
+        e.soa, g, kcoefs<MULTI>(co), n_groups, e.n, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }
@@ -285,7 +285,8 @@ template cudaError_t launch_stream_soa_grid<double>(const EnsView &, const GridA
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
     k_push_deposit_soa(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
-                       const __grid_constant__ Coefs<FP> co, const __grid_constant__ DepCoefs<FP> dc,
+                       const __grid_constant__ KCoefs<FP, MULTI> co,
+                       const __grid_constant__ DepCoefs<FP> dc,
                        const DepOut<FP> o, int64_t n_groups, int64_t n, double *partials) {
     constexpr int V = Vec<FP>::N;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
@@ -396,7 +397,7 @@ static cudaError_t dispatch_push_deposit(const EnsView &e, const GridArgs<FP> &g
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, BORIS_PD_MINB, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
     k_push_deposit_soa<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
-        e.soa, g, co, dc, o, n_groups, e.n, diag ? diag->partials : nullptr);
+        e.soa, g, kcoefs<MULTI>(co), dc, o, n_groups, e.n, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }
@@ -439,7 +440,7 @@ template cudaError_t launch_push_deposit_soa<double>(const EnsView &, const Grid
 // accesses, the same push_one arithmetic.
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void __launch_bounds__(kStreamThreads)
-    k_stream_soa_scalar(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ Coefs<FP> co,
+    k_stream_soa_scalar(SoaPtrs s, FieldSoaPtrs f, const __grid_constant__ KCoefs<FP, MULTI> co,
                         int64_t n, double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     if (MULTI) load_type_table(co, s_t);
@@ -486,13 +487,14 @@ static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const C
         grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
         if (DIAG && grid > diag->cap) grid = diag->cap;
         k_stream_soa_vec<FP, MULTI, DIAG>
-            <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, co, n_groups, e.n, partials);
+            <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, kcoefs<MULTI>(co), n_groups, e.n,
+                                                        partials);
     } else {
         const int64_t blocks = (e.n + kStreamThreads - 1) / kStreamThreads;
         grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
         if (DIAG && grid > diag->cap) grid = diag->cap;
         k_stream_soa_scalar<FP, MULTI, DIAG>
-            <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, co, e.n, partials);
+            <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, kcoefs<MULTI>(co), e.n, partials);
     }
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();

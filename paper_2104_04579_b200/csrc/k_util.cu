@@ -85,7 +85,7 @@ int64_t resident_grid(const void *kernel, int threads, int64_t work_blocks, int 
 // ---------------------------------------------------------------------------
 template <typename FP, int LAYOUT, bool MULTI>
 __global__ void __launch_bounds__(kStreamThreads)
-    k_kinetic_energy(EnsView e, const __grid_constant__ Coefs<FP> co, double *partials) {
+    k_kinetic_energy(EnsView e, const __grid_constant__ KCoefs<FP, MULTI> co, double *partials) {
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
     if (MULTI) load_type_table(co, s_t);
     double ke = 0.0, cnt = 0.0;
@@ -124,13 +124,13 @@ cudaError_t launch_kinetic_energy(const EnsView &e, const Coefs<FP> &co, bool mu
     if (grid > diag->cap) grid = diag->cap;
     const bool soa = e.layout == BORIS_LAYOUT_SOA;
     if (soa && multi)
-        k_kinetic_energy<FP, BORIS_LAYOUT_SOA, true><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, co, diag->partials);
+        k_kinetic_energy<FP, BORIS_LAYOUT_SOA, true><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, kcoefs<true>(co), diag->partials);
     else if (soa)
-        k_kinetic_energy<FP, BORIS_LAYOUT_SOA, false><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, co, diag->partials);
+        k_kinetic_energy<FP, BORIS_LAYOUT_SOA, false><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, kcoefs<false>(co), diag->partials);
     else if (multi)
-        k_kinetic_energy<FP, BORIS_LAYOUT_AOS, true><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, co, diag->partials);
+        k_kinetic_energy<FP, BORIS_LAYOUT_AOS, true><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, kcoefs<true>(co), diag->partials);
     else
-        k_kinetic_energy<FP, BORIS_LAYOUT_AOS, false><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, co, diag->partials);
+        k_kinetic_energy<FP, BORIS_LAYOUT_AOS, false><<<(unsigned)grid, kStreamThreads, 0, st>>>(e, kcoefs<false>(co), diag->partials);
     diag->written = grid;
     return cudaGetLastError();
 }

@@ -10,4 +10,5 @@ timeout 600 python scripts/bench_grid.py > $OUT/grid.jsonl 2> $OUT/grid.err; ech
 timeout 600 python scripts/bench_deposit.py > $OUT/dep.jsonl 2> $OUT/dep.err; echo "dep=$?" >> $OUT/rc.txt
 timeout 600 python scripts/pic_cycle.py > $OUT/pic.jsonl 2> $OUT/pic.err; echo "pic=$?" >> $OUT/rc.txt
 timeout 600 python scripts/pic_cycle.py --fused >> $OUT/pic.jsonl 2>> $OUT/pic.err
+timeout 300 python scripts/bench_launch.py > $OUT/launch.jsonl 2>> $OUT/err.log
 cat $OUT/rc.txt; tail -2 $OUT/pytest_gpu.log; grep -E "^FAILED" $OUT/pytest_gpu.log | head

@@ -111,7 +111,7 @@ def test_argument_validation_host_only(lb):
         lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP32, 1, [(1.0, 0.0)], 1.0)
     assert ei.value.status == lb.BORIS_E_INVALID_ARG
     with pytest.raises(lb.BorisError) as ei:   # too many types
-        lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP32, 1, [(1.0, 1.0)] * 33, 1.0)
+        lb.boris_ensemble_create(0, lb.BORIS_LAYOUT_SOA, lb.BORIS_FP32, 1, [(1.0, 1.0)] * 257, 1.0)
     assert ei.value.status == lb.BORIS_E_INVALID_ARG
     with pytest.raises(lb.BorisError) as ei:
         lb.boris_push(None, None, 1.0, 1)

@@ -360,6 +360,35 @@ def test_axis_aligned_specialisation_equals_generic_bitwise(cfg, layout, precisi
     assert torch.equal(da, db)
 
 
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_full_type_table_parity(layout, precision):
+    """BORIS_MAX_TYPES = 256 particle types (the paper's per-type table, L202-205;
+    SURVEY §8(a) a3: <= 256 entries) with charges and masses spread over two decades,
+    random type indices: one streaming step and 20 fused steps against the oracle
+    (c15), so every table entry and the shared-memory copy of the table are used."""
+    w = synth.config("C2")
+    g = torch.Generator().manual_seed(21)
+    nt = lb.BORIS_MAX_TYPES
+    qs = (torch.rand(nt, generator=g, dtype=torch.float64) * 2 - 1) * synth.E_CHARGE
+    ms = synth.M_ELECTRON * 10 ** (2 * torch.rand(nt, generator=g, dtype=torch.float64))
+    w.types = [(float(q), float(m)) for q, m in zip(qs, ms)]
+    w.type_mix = "random"
+    d, ens, field = build(w, layout, precision, N_SMALL)
+    assert int(d["type"].max()) > 200
+    ref = OracleRun(w, d, precision)
+    metric = C15()
+    for steps in (1, 20):
+        lb.boris_push(ens.handle, field, w.dt, steps)
+        ref.push(steps)
+        torch.cuda.synchronize()
+        r, p, _, st = gpu_state(ens)
+        assert torch.equal(st["type"], d["type"])
+        er, ep = metric("r", r, ref.pos), metric("p", p, ref.mom)
+        assert er <= TOL[precision] and ep <= TOL[precision], (steps, er, ep)
+    ens.close()
+
+
 def mdipole_workload():
     # m-dipole at P = 0.1 PW (PAPER.md L396-426, reading c12: A0 = k sqrt(3P/c)).
     w = synth.config("C4")
