@@ -119,12 +119,6 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
 #define BORIS_GRID_MINB 3
 #endif
 #define BORIS_GRID_BOUNDS __launch_bounds__(kStreamThreads, BORIS_GRID_MINB)
-#ifndef BORIS_GRID_REUSE
-#define BORIS_GRID_REUSE 0
-#endif
-#ifndef BORIS_GRID_PREFETCH
-#define BORIS_GRID_PREFETCH 0
-#endif
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void BORIS_GRID_BOUNDS
     k_stream_soa_grid(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
@@ -138,9 +132,6 @@ __global__ void BORIS_GRID_BOUNDS
     const FP *W = (const FP *)s.w;
     double ke = 0.0, cnt = 0.0;
     const int64_t stride = (int64_t)gridDim.x * kStreamThreads;
-#if BORIS_GRID_REUSE
-    GridCache<FP> gcache;  // consecutive (sorted: same-cell) particles reuse the records
-#endif
     struct State {
         Vec<FP> x, y, z, px, py, pz, w;
         int ty[V];
@@ -167,21 +158,12 @@ __global__ void BORIS_GRID_BOUNDS
     if (grp < n_groups) load(grp, cur);
     for (; grp < n_groups; grp += stride) {
         const int64_t i0 = grp * V;
-#if BORIS_GRID_PREFETCH
-        State nxt;
-        if (grp + stride < n_groups) load(grp + stride, nxt);
-#endif
         Vec<FP> gm;
         FP ex[V], ey[V], ez[V], bx[V], by[V], bz[V];
 #pragma unroll
         for (int j = 0; j < V; ++j)
-#if BORIS_GRID_REUSE
-            grid_gather_cached<FP>(g, cur.x.v[j], cur.y.v[j], cur.z.v[j], gcache, ex[j], ey[j],
-                                   ez[j], bx[j], by[j], bz[j]);
-#else
             grid_gather<FP>(g, cur.x.v[j], cur.y.v[j], cur.z.v[j], ex[j], ey[j], ez[j], bx[j],
                             by[j], bz[j]);
-#endif
 #pragma unroll
         for (int j = 0; j < V; ++j) {
             const TypeCoef<FP> tc = MULTI ? s_t[cur.ty[j]] : co.t[0];
@@ -201,11 +183,7 @@ __global__ void BORIS_GRID_BOUNDS
         cur.py.store(PY + i0);
         cur.pz.store(PZ + i0);
         gm.store(G + i0);
-#if BORIS_GRID_PREFETCH
-        cur = nxt;
-#else
         if (grp + stride < n_groups) load(grp + stride, cur);
-#endif
     }
     const int64_t tail0 = n_groups * V;
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail0) {
