@@ -93,6 +93,20 @@ __device__ __forceinline__ float md_radius(float r2) {
 }
 __device__ __forceinline__ double md_radius(double r2) { return __dsqrt_rn(r2); }
 
+// Closed-form branch of the radial functions (eq. 15, reading c11) from s = sin xi,
+// c = cos xi and i = 1/xi, factored so that each product is formed once:
+//   g1 = f1/xi   = i^2 (s i - c)
+//   g2 = f2/xi^2 = i^3 (3 (i (s i) - c i) - s)
+//   f3           = i (s + c i - (s i) i)
+// (f1 = s/xi^2 - c/xi, f2 = (3/xi^3 - 1/xi) s - 3c/xi^2, f3 = (1/xi - 1/xi^3) s + c/xi^2).
+template <typename FP>
+__device__ __forceinline__ void md_closed(FP sn, FP cs, FP ix, FP &g1, FP &g2, FP &f3) {
+    const FP a = b_mul(sn, ix), b = b_mul(cs, ix), i2 = b_mul(ix, ix);
+    g1 = b_mul(i2, b_add(a, -cs));
+    g2 = b_mul(b_mul(i2, ix), b_fma(FP(3), b_fma(ix, a, -b), -sn));
+    f3 = b_mul(ix, b_add(sn, b_fma(-a, ix, b)));
+}
+
 template <typename FP>
 __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
     if (xi < MdBranch<FP>::xi_star) {
@@ -127,12 +141,7 @@ __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
             sincos(xi, &sn, &cs);
             ix = __drcp_rn(xi);  // == 1.0 / xi (both correctly rounded), no division
         }
-        const FP ix2 = ix * ix, ix3 = ix2 * ix;
-        const FP f1 = sn * ix2 - cs * ix;
-        const FP f2 = (FP(3) * ix3 - ix) * sn - FP(3) * cs * ix2;
-        f3 = (ix - ix3) * sn + cs * ix2;
-        g1 = f1 * ix;
-        g2 = f2 * ix2;
+        md_closed<FP>(sn, cs, ix, g1, g2, f3);
     }
 }
 
@@ -176,12 +185,7 @@ __device__ __forceinline__ void md_radial_r2(const AnalyticArgs<FP> &fa, FP r2, 
             const float r = __fmaf_rn(-q, -1.7484555e-07f, __fmaf_rn(-q, 6.2831855f, xi));
             float sn, cs;
             __sincosf(r, &sn, &cs);
-            const float ix2 = ix * ix, ix3 = ix2 * ix;
-            const float f1 = sn * ix2 - cs * ix;
-            const float f2 = (3.f * ix3 - ix) * sn - 3.f * cs * ix2;
-            f3 = (ix - ix3) * sn + cs * ix2;
-            g1 = f1 * ix;
-            g2 = f2 * ix2;
+            md_closed<float>(sn, cs, ix, g1, g2, f3);
         }
         return;
     }
@@ -564,7 +568,8 @@ __global__ void __launch_bounds__(kFusedThreads)
                 dz = b_fma(ct, uz, dz);
             };
             // full windows of the short-bodied fields run as straight-line code (measured
-            // +4 % on C4); the long m-dipole / grid bodies stay rolled (unrolled: -15 %).
+            // +4 % on C4); the long m-dipole / grid bodies stay rolled (unrolled: -15 %;
+            // unrolled by 2: m-dipole -0.5..2 %, grid -5 %).
             constexpr bool kUnroll = FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE;
             if (kUnroll && m == kFlush) {
 #pragma unroll
