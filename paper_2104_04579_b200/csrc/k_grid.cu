@@ -55,6 +55,78 @@ cudaError_t launch_grid_pack(int precision, int64_t ncell, int nx, const void *c
     return cudaGetLastError();
 }
 
+// SoA permutation by particle records.  A permutation from random order gathers
+// every array at random indices; a 4 B gather costs a whole DRAM access, so eight
+// separate array gathers moved ~740 B per particle (ncu, 10^7, random order).
+// Instead: (1) k_pack_soa writes each particle's present arrays as one record of
+// RS FP slots (x y z px py pz [w] [g] [type]) with coalesced reads; (2)
+// k_unpack_soa reads record perm[i] (RS adjacent slots: 1-2 sectors) and writes
+// slot a to array a at i, coalesced, straight into the ensemble's own arrays (the
+// records are the only copy, so no copy-back pass).  From sorted order the record
+// reads are sequential too, so the traffic is the same as gather + copy-back.
+struct PermPlan {
+    void *arr[8];  // present FP arrays in record-slot order
+    int nf;        // number of FP slots before the type slot
+    int16_t *type; // null: no type slot
+    int rs;        // record stride in FP slots
+};
+
+static PermPlan perm_plan(const SoaPtrs &s) {
+    PermPlan p{};
+    void *all[8] = {s.x, s.y, s.z, s.px, s.py, s.pz, s.w, s.g};
+    for (int a = 0; a < 8; ++a)
+        if (all[a]) p.arr[p.nf++] = all[a];
+    p.type = s.type;
+    p.rs = p.nf + (s.type ? 1 : 0);
+    return p;
+}
+
+// Records whose size is a multiple of 16 B (x y z px py pz w g without a type slot)
+// are written straight from registers with 16 B vector stores by the first radix
+// histogram pass (k_rs_hist<.., PACK>).  Otherwise the records of a 256-particle tile
+// are assembled in shared memory (thread t writes
+// slots t*RS + a; RS = 9 is odd, so fp32 writes are conflict-free) and leave as
+// contiguous 16 B vector stores: every written sector is written whole either way
+// (scalar stores at a 36 B lane stride took 3x the time of the traffic).
+constexpr int kPackTile = 256;
+
+template <typename FP>
+__global__ void __launch_bounds__(kPackTile)
+    k_pack_soa(const __grid_constant__ PermPlan p, int64_t n, FP *rec) {
+    using W = typename std::conditional<sizeof(FP) == 4, uint32_t, unsigned long long>::type;
+    extern __shared__ __align__(16) unsigned char pack_smem[];
+    FP *tile = reinterpret_cast<FP *>(pack_smem);
+    const int64_t ntiles = (n + kPackTile - 1) / kPackTile;
+    const int t = threadIdx.x;
+    for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
+        const int64_t i0 = tb * kPackTile;
+        const int cnt = (int)(n - i0 < kPackTile ? n - i0 : kPackTile);
+        if (t < cnt) {
+            const int64_t i = i0 + t;
+            FP v[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (a < p.nf) v[a] = ((const FP *)p.arr[a])[i];
+            FP *r = tile + t * p.rs;
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (a < p.nf) r[a] = v[a];
+            if (p.type) reinterpret_cast<W *>(r)[p.nf] = (W)(uint16_t)p.type[i];
+        }
+        __syncthreads();
+        // cnt * rs FP values, contiguous at rec + i0 * rs (16 B aligned: i0 * rs * sizeof(FP)
+        // is a multiple of 256 * 4 B)
+        const int64_t words = (int64_t)cnt * p.rs;
+        const int nvec = (int)(words * sizeof(FP) / 16);
+        uint4 *dst = reinterpret_cast<uint4 *>(rec + i0 * p.rs);
+        const uint4 *src = reinterpret_cast<const uint4 *>(tile);
+        for (int k = t; k < nvec; k += kPackTile) dst[k] = src[k];
+        for (int64_t k = (int64_t)nvec * 16 / sizeof(FP) + t; k < words; k += kPackTile)
+            rec[i0 * p.rs + k] = tile[k];
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Stable LSD radix sort of the particles' cell keys, digits of up to 10 bits
 // (a 64^3 grid's 18-bit keys take 2 passes of 9 bits).  Tile = 256 threads x 8
@@ -73,10 +145,14 @@ constexpr int kRsMaxBins = 1 << kRsMaxBits;
 
 // Histogram of one digit per tile, written digit-major: hist[d * nb + tile].
 // KEYS: compute the key of particle i from its position and store it.
-template <typename FP, bool KEYS>
+// PACK (pass 0, SoA records that are a 16 B multiple): the same threads also write
+// each particle's packed record (16 B vector stores), so the permutation's pack
+// costs no separate read of the positions and no launch.
+template <typename FP, bool KEYS, bool PACK = false>
 __global__ void __launch_bounds__(kRsThreads)
     k_rs_hist(EnsView e, const __grid_constant__ GridArgs<FP> g, uint32_t *keys, int64_t n,
-              int shift, int bins, uint32_t *hist, int64_t nb) {
+              int shift, int bins, uint32_t *hist, int64_t nb,
+              const __grid_constant__ PermPlan plan, FP *rec) {
     constexpr int RB = sizeof(FP) == 4 ? BORIS_AOS_RECORD_BYTES_FP32 : BORIS_AOS_RECORD_BYTES_FP64;
     __shared__ uint32_t cnt[kRsMaxBins];
     for (int b = threadIdx.x; b < bins; b += kRsThreads) cnt[b] = 0;
@@ -102,6 +178,22 @@ __global__ void __launch_bounds__(kRsThreads)
                 }
                 key = grid_cell<FP>(g, x, y, z);
                 keys[i] = key;
+                if constexpr (PACK) {  // plan.arr[0..2] are x, y, z
+                    constexpr int V = 16 / sizeof(FP);
+                    FP v[8];
+                    v[0] = x; v[1] = y; v[2] = z;
+#pragma unroll
+                    for (int a = 3; a < 8; ++a)
+                        if (a < plan.nf) v[a] = ((const FP *)plan.arr[a])[i];
+                    uint4 *r = reinterpret_cast<uint4 *>(rec + i * plan.rs);
+#pragma unroll
+                    for (int k = 0; k < 8 / V; ++k)
+                        if (k * V < plan.nf) {
+                            uint4 u;
+                            memcpy(&u, v + k * V, 16);
+                            r[k] = u;
+                        }
+                }
             } else {
                 key = keys[i];
             }
@@ -187,7 +279,10 @@ constexpr int kScanChunk = kScanThreads * kScanItems;
 
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_chunks(uint32_t *data, int64_t len, uint32_t *chunk_tot) {
-    __shared__ uint32_t s[kScanThreads];
+    // thread sums of 4 items, a warp-shuffle inclusive scan, the 32 warp totals
+    // scanned by warp 0: two block barriers
+    __shared__ uint32_t s_w[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t c0 = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
     uint32_t v[kScanItems], sum = 0;
 #pragma unroll
@@ -195,21 +290,31 @@ __global__ void __launch_bounds__(kScanThreads)
         v[k] = (c0 + k < len) ? data[c0 + k] : 0u;
         sum += v[k];
     }
-    s[threadIdx.x] = sum;
-    __syncthreads();
-    for (int off = 1; off < kScanThreads; off <<= 1) {  // Hillis-Steele inclusive
-        const uint32_t add = threadIdx.x >= (unsigned)off ? s[threadIdx.x - off] : 0u;
-        __syncthreads();
-        s[threadIdx.x] += add;
-        __syncthreads();
+    uint32_t inc = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += t;
     }
-    uint32_t run = s[threadIdx.x] - sum;  // exclusive prefix of this thread
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = s_w[lane];  // kScanThreads / 32 == 32 warps
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, w, off);
+            if (lane >= off) w += t;
+        }
+        s_w[lane] = w;
+    }
+    __syncthreads();
+    uint32_t run = inc - sum + (warp > 0 ? s_w[warp - 1] : 0u);  // exclusive prefix
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         if (c0 + k < len) data[c0 + k] = run;
         run += v[k];
     }
-    if (threadIdx.x == kScanThreads - 1 && chunk_tot) chunk_tot[blockIdx.x] = s[threadIdx.x];
+    if (threadIdx.x == kScanThreads - 1 && chunk_tot) chunk_tot[blockIdx.x] = s_w[31];
 }
 
 __global__ void k_scan_add(uint32_t *data, int64_t len, const uint32_t *chunk_off) {
@@ -255,98 +360,6 @@ __global__ void k_gather_bytes(const unsigned char *in, unsigned char *out, cons
 #pragma unroll
             for (int k = 0; k < BYTES / 2; ++k) d[k] = s[k];
         }
-    }
-}
-
-// SoA permutation by particle records.  A permutation from random order gathers
-// every array at random indices; a 4 B gather costs a whole DRAM access, so eight
-// separate array gathers moved ~740 B per particle (ncu, 10^7, random order).
-// Instead: (1) k_pack_soa writes each particle's present arrays as one record of
-// RS FP slots (x y z px py pz [w] [g] [type]) with coalesced reads; (2)
-// k_unpack_soa reads record perm[i] (RS adjacent slots: 1-2 sectors) and writes
-// slot a to array a at i, coalesced, straight into the ensemble's own arrays (the
-// records are the only copy, so no copy-back pass).  From sorted order the record
-// reads are sequential too, so the traffic is the same as gather + copy-back.
-struct PermPlan {
-    void *arr[8];  // present FP arrays in record-slot order
-    int nf;        // number of FP slots before the type slot
-    int16_t *type; // null: no type slot
-    int rs;        // record stride in FP slots
-};
-
-static PermPlan perm_plan(const SoaPtrs &s) {
-    PermPlan p{};
-    void *all[8] = {s.x, s.y, s.z, s.px, s.py, s.pz, s.w, s.g};
-    for (int a = 0; a < 8; ++a)
-        if (all[a]) p.arr[p.nf++] = all[a];
-    p.type = s.type;
-    p.rs = p.nf + (s.type ? 1 : 0);
-    return p;
-}
-
-// Records whose size is a multiple of 16 B (x y z px py pz w g without a type slot)
-// are written straight from registers with 16 B vector stores.  Otherwise the
-// records of a 256-particle tile are assembled in shared memory (thread t writes
-// slots t*RS + a; RS = 9 is odd, so fp32 writes are conflict-free) and leave as
-// contiguous 16 B vector stores: every written sector is written whole either way
-// (scalar stores at a 36 B lane stride took 3x the time of the traffic).
-constexpr int kPackTile = 256;
-
-template <typename FP>
-__global__ void __launch_bounds__(kPackTile)
-    k_pack_soa_vec(const __grid_constant__ PermPlan p, int64_t n, FP *rec) {
-    constexpr int V = 16 / sizeof(FP);  // FP per 16 B vector
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        FP v[8];
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-            if (a < p.nf) v[a] = ((const FP *)p.arr[a])[i];
-        uint4 *r = reinterpret_cast<uint4 *>(rec + i * p.rs);
-#pragma unroll
-        for (int k = 0; k < 8 / V; ++k)
-            if (k * V < p.nf) {
-                uint4 u;
-                memcpy(&u, v + k * V, 16);
-                r[k] = u;
-            }
-    }
-}
-
-template <typename FP>
-__global__ void __launch_bounds__(kPackTile)
-    k_pack_soa(const __grid_constant__ PermPlan p, int64_t n, FP *rec) {
-    using W = typename std::conditional<sizeof(FP) == 4, uint32_t, unsigned long long>::type;
-    extern __shared__ __align__(16) unsigned char pack_smem[];
-    FP *tile = reinterpret_cast<FP *>(pack_smem);
-    const int64_t ntiles = (n + kPackTile - 1) / kPackTile;
-    const int t = threadIdx.x;
-    for (int64_t tb = blockIdx.x; tb < ntiles; tb += gridDim.x) {
-        const int64_t i0 = tb * kPackTile;
-        const int cnt = (int)(n - i0 < kPackTile ? n - i0 : kPackTile);
-        if (t < cnt) {
-            const int64_t i = i0 + t;
-            FP v[8];
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-                if (a < p.nf) v[a] = ((const FP *)p.arr[a])[i];
-            FP *r = tile + t * p.rs;
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-                if (a < p.nf) r[a] = v[a];
-            if (p.type) reinterpret_cast<W *>(r)[p.nf] = (W)(uint16_t)p.type[i];
-        }
-        __syncthreads();
-        // cnt * rs FP values, contiguous at rec + i0 * rs (16 B aligned: i0 * rs * sizeof(FP)
-        // is a multiple of 256 * 4 B)
-        const int64_t words = (int64_t)cnt * p.rs;
-        const int nvec = (int)(words * sizeof(FP) / 16);
-        uint4 *dst = reinterpret_cast<uint4 *>(rec + i0 * p.rs);
-        const uint4 *src = reinterpret_cast<const uint4 *>(tile);
-        for (int k = t; k < nvec; k += kPackTile) dst[k] = src[k];
-        for (int64_t k = (int64_t)nvec * 16 / sizeof(FP) + t; k < words; k += kPackTile)
-            rec[i0 * p.rs + k] = tile[k];
-        __syncthreads();
     }
 }
 
@@ -425,14 +438,32 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     unsigned char *tmp = (unsigned char *)(hist + (size_t)bins * nb);
     tmp = (unsigned char *)(((uintptr_t)tmp + 255) & ~(uintptr_t)255);
 
+    // SoA: packed particle records for the permutation (PermPlan); written by the
+    // first histogram pass when they are a 16 B multiple, else by k_pack_soa
+    const bool soa = e.layout == BORIS_LAYOUT_SOA;
+    PermPlan plan{};
+    FP *rec = nullptr;
+    bool fused_pack = false;
+    if (soa) {
+        plan = perm_plan(e.soa);
+        fused_pack = !plan.type && plan.rs * sizeof(FP) % 16 == 0;
+        if ((err = scratch_alloc((void **)&rec, (size_t)n * plan.rs * sizeof(FP), st)) !=
+            cudaSuccess) {
+            scratch_free(buf, st);
+            return err;
+        }
+    }
     for (int p = 0; p < passes && err == cudaSuccess; ++p) {
         const int shift = dbits * p;
-        if (p == 0)
+        if (p == 0 && fused_pack)
+            k_rs_hist<FP, true, true><<<(unsigned)nb, kRsThreads, 0, st>>>(
+                e, g, k0, n, shift, bins, hist, nb, plan, rec);
+        else if (p == 0)
             k_rs_hist<FP, true><<<(unsigned)nb, kRsThreads, 0, st>>>(e, g, k0, n, shift, bins,
-                                                                   hist, nb);
+                                                                   hist, nb, plan, rec);
         else
             k_rs_hist<FP, false><<<(unsigned)nb, kRsThreads, 0, st>>>(e, g, k0, n, shift, bins,
-                                                                    hist, nb);
+                                                                    hist, nb, plan, rec);
         if ((err = cudaGetLastError()) != cudaSuccess) break;
         if ((err = exclusive_scan(hist, (int64_t)bins * nb, st)) != cudaSuccess) break;
         const bool last = p == passes - 1;
@@ -446,28 +477,22 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
     }
     // v0 = sorted original indices: apply to every particle array
     if (err == cudaSuccess) {
-        if (e.layout == BORIS_LAYOUT_SOA) {
-            // pack records, then gather them through the permutation into the arrays
-            const PermPlan plan = perm_plan(e.soa);
-            FP *rec = nullptr;
-            err = scratch_alloc((void **)&rec, (size_t)n * plan.rs * sizeof(FP), st);
-            if (err == cudaSuccess) {
+        if (soa) {
+            // gather the packed records through the permutation into the arrays
+            if (!fused_pack) {
                 const size_t smem = (size_t)kPackTile * plan.rs * sizeof(FP);
-                if (!plan.type && plan.rs * sizeof(FP) % 16 == 0)
-                    k_pack_soa_vec<FP><<<grid1d(n), kPackTile, 0, st>>>(plan, n, rec);
-                else
-                    k_pack_soa<FP><<<grid1d(n), kPackTile, smem, st>>>(plan, n, rec);
+                k_pack_soa<FP><<<grid1d(n), kPackTile, smem, st>>>(plan, n, rec);
                 err = cudaGetLastError();
-                if (err == cudaSuccess) {
-                    k_unpack_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(plan, v0, n, rec);
-                    err = cudaGetLastError();
-                }
-                scratch_free(rec, st);
+            }
+            if (err == cudaSuccess) {
+                k_unpack_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(plan, v0, n, rec);
+                err = cudaGetLastError();
             }
         } else {
             err = permute_array<RB>(e.aos, tmp, v0, n, st);
         }
     }
+    if (rec) scratch_free(rec, st);
     scratch_free(buf, st);
     return err;
 }
