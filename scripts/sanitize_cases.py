@@ -90,12 +90,12 @@ def main():
                                           [L / (g + 2), L / (g + 1), L / g],
                                           *(c.data_ptr() for c in comps))
         J = [torch.zeros((g, g + 1, g + 2), device="cuda", dtype=dt) for _ in range(3)]
-        for n in (13, 3 * 2048 + 77):
+        for n, types in ((13, THREE), (3 * 2048 + 77, THREE), (3 * 2048 + 77, [synth.ELECTRON])):
             w = synth.config("C2", n=n)
-            w.types = THREE
+            w.types = types
             w.type_mix = "random"
             for cls in (SoaEnsemble, AosEnsemble):
-                e = cls(n, prec, THREE, w.light_velocity)
+                e = cls(n, prec, types, w.light_velocity)
                 e.fill(w.generate())
                 e.wrap()
                 lb.boris_ensemble_sort_by_cell(e.handle, grid)
@@ -120,7 +120,38 @@ def main():
                 lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 0)
                 torch.cuda.synchronize()
                 e.close()
+        # wrapped SoA one element off alignment (scalar / warp-run paths), no weight
+        n = 2 * 2048 + 45
+        big = SoaEnsemble(n + 1, prec, THREE, synth.C_LIGHT)
+        wv = synth.config("C2", n=n + 1)
+        wv.types = THREE
+        wv.type_mix = "random"
+        big.fill(wv.generate())
+        keys = ("x", "y", "z", "px", "py", "pz")
+        h = lb.boris_ensemble_wrap_soa(0, lb.BORIS_MEMORY_DEVICE, prec, n,
+                                       *(big.t[k][1:].data_ptr() for k in keys), None,
+                                       big.t["gamma"][1:].data_ptr(), big.t["type"][1:].data_ptr(),
+                                       THREE, synth.C_LIGHT)
+        lb.boris_ensemble_sort_by_cell(h, grid)
+        lb.boris_deposit_current(h, grid, wv.dt, *(j.data_ptr() for j in J))
+        lb.boris_push_deposit(h, grid, wv.dt, *(j.data_ptr() for j in J), dp)
+        torch.cuda.synchronize()
+        lb.boris_ensemble_destroy(h)
+        big.close()
         lb.boris_field_destroy(grid)
+    # the full 256-entry type table (shared-memory copy in every multi-type kernel)
+    many = [(synth.E_CHARGE * (1 - 2 * (i % 2)), synth.M_ELECTRON * (1 + i)) for i in range(256)]
+    w = synth.config("C2", n=4096 + 7)
+    w.types = many
+    w.type_mix = "random"
+    for cls in (SoaEnsemble, AosEnsemble):
+        e = cls(w.n, lb.BORIS_FP32, many, w.light_velocity)
+        e.fill(w.generate())
+        e.wrap()
+        lb.boris_push_diag(e.handle, e.field, w.dt, 1, dp)
+        lb.boris_push_diag(e.handle, e.field, w.dt, 4, dp)
+        torch.cuda.synchronize()
+        e.close()
     # host-resident pipeline, several chunks
     lb.boris_set_option(lb.BORIS_OPT_HOST_CHUNK, 2048)
     w = synth.config("C5", n=5000)
