@@ -159,6 +159,23 @@ struct DepositRun {
             }
     }
 
+    // One particle prepared by WarpRun<FP>::prepare (unwrapped cell, node weights,
+    // q w v / volume): the cell test and the 24 FMA only, so a caller can prepare
+    // several particles first (independent chains) and accumulate them after.
+    template <typename Part>
+    __device__ __forceinline__ void add_part(const GridArgs<FP> &g, const DepOut<FP> &o,
+                                             const Part &p) {
+        if (nb == kNoNode || p.l[0] != fl[0] || p.l[1] != fl[1] || p.l[2] != fl[2]) {
+            flush(o);
+            fl[0] = p.l[0]; fl[1] = p.l[1]; fl[2] = p.l[2];
+            nb = base_node(g, o, p.l);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) acc[q][d] = b_fma(p.sw[q], p.qv[d], acc[q][d]);
+    }
+
     // End of a warp tile (all 32 lanes): lanes holding the same open cell in
     // consecutive lanes (contiguous when sorted) are summed with a segmented
     // scan; every lane but each segment's last drops its cell, so the following

@@ -645,6 +645,9 @@ constexpr int kDepTile = 32 * kDepK;
 #ifndef BORIS_DEP_DIRECT_MINB
 #define BORIS_DEP_DIRECT_MINB 2
 #endif
+#ifndef BORIS_DEP_PREP
+#define BORIS_DEP_PREP 1
+#endif
 __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
     k_deposit_runs(EnsView e, const __grid_constant__ GridArgs<float> g,
                    const __grid_constant__ DepCoefs<float> dc, const DepOut<float> o) {
@@ -690,6 +693,24 @@ __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
         }
         DepositRun<float> run;
         run.reset();
+#if BORIS_DEP_PREP
+        if (i0 + kDepK <= e.n) {
+            // groups of 4: the four particles' weights first (independent chains),
+            // then the cell tests and accumulations
+#pragma unroll
+            for (int h = 0; h < kDepK; h += 4) {
+                WarpRun<float>::Part pp[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    WarpRun<float>::prepare(g, dc.t[multi ? rty[h + j] : 0], dc.half_dt,
+                                            rv[0][h + j], rv[1][h + j], rv[2][h + j],
+                                            rv[3][h + j], rv[4][h + j], rv[5][h + j],
+                                            rv[6][h + j], pp[j]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) run.add_part(g, o, pp[j]);
+            }
+        } else
+#endif
 #pragma unroll
         for (int j = 0; j < kDepK; ++j) {
             if (i0 + j >= e.n) break;

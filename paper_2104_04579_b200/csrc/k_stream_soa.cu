@@ -257,6 +257,9 @@ template cudaError_t launch_stream_soa_grid<double>(const EnsView &, const GridA
 // order of its float atomics.  Warp-uniform grid-stride loop (every lane takes
 // part in the end-of-group segmented merge).
 // ---------------------------------------------------------------------------
+#ifndef BORIS_PD_PREP
+#define BORIS_PD_PREP 1
+#endif
 #ifndef BORIS_PD_MINB
 #define BORIS_PD_MINB 2
 #endif
@@ -328,10 +331,22 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             gm.store(G + i0);
             // deposition of the new state (measured: recomputing 1/gamma from the
             // stored p after the stores beats carrying the push's u and 1/gamma)
+#if BORIS_PD_PREP
+            {   // the V particles' weights first (independent chains), then accumulate
+                typename WarpRun<FP>::Part pp[V];
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    WarpRun<FP>::prepare(g, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j],
+                                         y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], w.v[j], pp[j]);
+#pragma unroll
+                for (int j = 0; j < V; ++j) run.add_part(g, o, pp[j]);
+            }
+#else
 #pragma unroll
             for (int j = 0; j < V; ++j)
                 run.add(g, o, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j], y.v[j], z.v[j],
                         px.v[j], py.v[j], pz.v[j], w.v[j]);
+#endif
         }
         if constexpr (kTransposedMergePD<FP>) {
             run.merge_flush(o, s_merge[threadIdx.x >> 5], lane);
