@@ -295,10 +295,14 @@ boris_status boris_ensemble_sort_by_cell(boris_ensemble *ens, const boris_field 
  * (r^{n+1}, p^{n+1/2}), deposit q w v^{n+1/2} of every particle at its half-step
  * position r^{n+1/2} = r^{n+1} - (dt/2) v^{n+1/2} onto the nodes of `grid` with the
  * CIC form factor, divided by the cell volume (current density, statA/cm^2).
- * Jx, Jy, Jz: DEVICE arrays of nx*ny*nz FP (node (i,j,k) at (k*ny+j)*nx+i), zeroed
- * and then accumulated by this call.  Hardware atomics: the summation order
- * varies run to run (results reproducible to rounding, not bitwise).
- * Device ensembles; grid precision and device must match (MISMATCH).  Asynchronous.
+ * Jx, Jy, Jz: DEVICE arrays of nx*ny*nz FP (node (i,j,k) at (k*ny+j)*nx+i),
+ * overwritten with the result.  The atomics accumulate into a stream-ordered
+ * scratch of (nx+1)(ny+1)(nz+1) nodes (16 B per node in fp32, 24 B in fp64; the
+ * +1 layers are periodic ghosts) from the library's memory pool, folded into J at
+ * the end.  Hardware atomics: the summation order varies run to run (results
+ * reproducible to rounding, not bitwise).  Device ensembles; grid precision and
+ * device must match (MISMATCH); OUT_OF_MEMORY if the scratch cannot be allocated.
+ * Asynchronous.
  */
 boris_status boris_deposit_current(const boris_ensemble *ens, const boris_field *grid, double dt,
                                    void *Jx, void *Jy, void *Jz, void *stream);
@@ -311,11 +315,12 @@ boris_status boris_deposit_current(const boris_ensemble *ens, const boris_field 
  * same grid (as boris_deposit_current(ens, grid, dt, Jx, Jy, Jz, stream)), in one
  * kernel for 16 B-aligned SoA ensembles (r, p and w are read once), else as the
  * two launches.  The ensemble state is bitwise the push's; J (DEVICE, nx*ny*nz FP
- * each, zeroed first) equals the separate deposition up to the order of its
- * float atomics.  d_diag (DEVICE, 2 doubles, or NULL): {sum KE, N} after the step,
+ * each, overwritten; the same scratch as boris_deposit_current) equals the
+ * separate deposition up to the order of its float atomics.  d_diag (DEVICE, 2 doubles, or NULL): {sum KE, N} after the step,
  * as boris_push_diag.  The ensemble time advances by dt.  Errors: INVALID_ARG
  * (NULL ens/grid/J, non-grid field, dt not finite), MISMATCH (precision or
- * device), UNSUPPORTED (host-resident ensemble), CUDA.  Asynchronous.
+ * device), UNSUPPORTED (host-resident ensemble), OUT_OF_MEMORY (scratch), CUDA.
+ * Asynchronous.
  */
 boris_status boris_push_deposit(boris_ensemble *ens, const boris_field *grid, double dt,
                                 void *Jx, void *Jy, void *Jz, double *d_diag, void *stream);
