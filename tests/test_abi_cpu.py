@@ -119,6 +119,35 @@ def test_argument_validation_host_only(lb):
     assert "NULL" in lb.boris_last_error()
 
 
+def test_options_are_abi_calls_not_environment(lb):
+    """boris_set_option / boris_get_option (host only, no device needed): defaults,
+    round trip, validation.  The library reads no environment variables."""
+    assert lb.boris_get_option(lb.BORIS_OPT_FUSED_GENERIC) == 0
+    chunk0 = lb.boris_get_option(lb.BORIS_OPT_HOST_CHUNK)
+    assert chunk0 == 4 << 20
+    try:
+        lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 1)
+        assert lb.boris_get_option(lb.BORIS_OPT_FUSED_GENERIC) == 1
+        lb.boris_set_option(lb.BORIS_OPT_HOST_CHUNK, 4096)
+        assert lb.boris_get_option(lb.BORIS_OPT_HOST_CHUNK) == 4096
+        for opt, bad in ((lb.BORIS_OPT_FUSED_GENERIC, 2), (lb.BORIS_OPT_HOST_CHUNK, 1023),
+                         (99, 0)):
+            with pytest.raises(lb.BorisError) as ei:
+                lb.boris_set_option(opt, bad)
+            assert ei.value.status == lb.BORIS_E_INVALID_ARG
+        with pytest.raises(lb.BorisError):
+            lb.boris_get_option(99)
+    finally:
+        lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 0)
+        lb.boris_set_option(lb.BORIS_OPT_HOST_CHUNK, chunk0)
+    # (the static CUDA runtime linked into libboris.so reads CUDA_* variables itself;
+    # libboris' own sources never call getenv)
+    import glob
+    csrc = os.path.join(os.path.dirname(lb.LIB_PATH), "csrc")
+    for f in glob.glob(os.path.join(csrc, "*.cu")) + glob.glob(os.path.join(csrc, "*.cuh")):
+        assert "getenv(" not in open(f).read(), f
+
+
 def test_field_handles_validate(lb):
     f = lb.boris_field_create_uniform([1, 2, 3], [0, 0, 1])
     lb.boris_field_destroy(f)
