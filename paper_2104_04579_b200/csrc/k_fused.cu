@@ -150,14 +150,15 @@ __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
 // series in xi^2 (no square root), and the closed form takes 1/xi = rsqrt(xi^2) from
 // one MUFU rsqrt and xi = xi^2 / xi -- one MUFU fewer than R = sqrt(r^2), xi = k R,
 // 1/xi = rcp(xi); the branch test xi < 1.5 becomes xi^2 < 2.25 (reading c13).  fp64
-// (and BORIS_PRECISE_MATH) use R = sqrt(r^2), xi = k R.
+// likewise with the double rsqrt (xi^2 < 1); BORIS_PRECISE_MATH uses R = sqrt(r^2),
+// xi = k R with correctly rounded square root and reciprocal.
 template <typename FP>
 __device__ __forceinline__ bool md_taylor(const AnalyticArgs<FP> &fa, FP r2) {
 #ifndef BORIS_PRECISE_MATH
-    if constexpr (sizeof(FP) == 4)
-        return b_mul(fa.k2, r2) < MdBranch<FP>::xi_star * MdBranch<FP>::xi_star;
-#endif
+    return b_mul(fa.k2, r2) < MdBranch<FP>::xi_star * MdBranch<FP>::xi_star;
+#else
     return b_mul(fa.k, md_radius(r2)) < MdBranch<FP>::xi_star;
+#endif
 }
 template <typename FP>
 __device__ __forceinline__ void md_radial_r2(const AnalyticArgs<FP> &fa, FP r2, FP &g1, FP &g2,
@@ -186,6 +187,30 @@ __device__ __forceinline__ void md_radial_r2(const AnalyticArgs<FP> &fa, FP r2, 
             float sn, cs;
             __sincosf(r, &sn, &cs);
             md_closed<float>(sn, cs, ix, g1, g2, f3);
+        }
+        return;
+    } else {
+        // fp64: the same from xi^2, with the double rsqrt (1 ulp) in place of the
+        // correctly rounded sqrt and reciprocal (two long software sequences)
+        const double x2 = b_mul(fa.k2, r2);
+        if (x2 < MdBranch<double>::xi_star * MdBranch<double>::xi_star) {
+            constexpr int T = MdBranch<double>::terms;
+            double j0 = c_md.j0[T - 1], j1x = c_md.j1x[T - 1], s2 = c_md.g2[T - 1];
+#pragma unroll
+            for (int n = T - 2; n >= 0; --n) {
+                j0 = j0 * x2 + c_md.j0[n];
+                j1x = j1x * x2 + c_md.j1x[n];
+            }
+#pragma unroll
+            for (int n = T - 2; n >= 1; --n) s2 = s2 * x2 + c_md.g2[n];
+            g1 = j1x;
+            g2 = s2;
+            f3 = j0 - j1x;
+        } else {
+            const double ix = rsqrt(x2), xi = b_mul(x2, ix);
+            double sn, cs;
+            sincos(xi, &sn, &cs);
+            md_closed<double>(sn, cs, ix, g1, g2, f3);
         }
         return;
     }
