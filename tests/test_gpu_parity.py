@@ -1158,6 +1158,109 @@ def test_sort_wrapped_arrays_with_optional_components(precision, has_w, has_type
     lb.boris_field_destroy(h)
 
 
+def _grid64(precision):
+    """The bench scripts' PIC grid: 64^3 nodes over a 1.5-lambda periodic box."""
+    g = 64
+    L = 1.5 * synth.LAMBDA0
+    dt_ = torch.float32 if precision == "fp32" else torch.float64
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    comps = [(torch.randn((g, g, g), generator=gen, device="cuda", dtype=torch.float64)
+              * 80 * synth.E_UNIT).to(dt_).contiguous() for _ in range(6)]
+    h = lb.boris_field_create_grid(0, PREC[precision], g, g, g, [-L / 2] * 3, [L / g] * 3,
+                                   *(c.data_ptr() for c in comps))
+    params = [-L / 2] * 3 + [L / g] * 3 + [g, g, g]
+    return h, params, comps
+
+
+def test_full_size_sort_and_deposition_pic_workload():
+    """The PIC benchmark workload at its full size (10^7 fp32 C2 particles, 64^3 grid,
+    the configuration scripts/bench_grid.py and bench_deposit.py time): the sort from
+    random order is a stable permutation (ids carried exactly in weight + gamma) that
+    orders the cells, and the deposition of the sorted ensemble equals the oracle's
+    within the summation bound (tol x sum |q w v| / volume per component)."""
+    h, params, comps = _grid64("fp32")
+    w = synth.config("C2", n=10_000_000)
+    n = w.n
+    ens = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity, with_fields=False)
+    ens.fill(w.generate(0, n, device="cuda"))
+    ids = torch.arange(n, device="cuda", dtype=torch.int64)
+    ens.t["weight"].copy_((ids % 4096).to(torch.float32) + 1.0)   # exact in fp32
+    ens.t["gamma"].copy_((ids // 4096).to(torch.float32))
+    ens.wrap()
+    before = {k: ens.t[k].clone() for k in ("x", "y", "z", "px", "py", "pz")}
+    lb.boris_ensemble_sort_by_cell(ens.handle, h)
+    torch.cuda.synchronize()
+    got = (ens.t["gamma"].to(torch.int64) * 4096 + ens.t["weight"].to(torch.int64) - 1)
+    assert torch.equal(torch.sort(got).values, ids)                 # a permutation
+    for k, v in before.items():
+        assert torch.equal(ens.t[k], v[got]), k                      # records moved whole
+    g = 64
+    cell = [torch.floor((ens.t[k].double() - params[a]) / params[3 + a]).long() % g
+            for a, k in enumerate(("x", "y", "z"))]
+    key = (cell[2] * g + cell[1]) * g + cell[0]
+    dk = key[1:] - key[:-1]
+    assert (dk >= 0).double().mean().item() > 1 - 1e-4
+    same = dk == 0
+    assert ((got[1:] - got[:-1])[same] > 0).double().mean().item() > 1 - 1e-4  # stable
+    # deposition of the sorted ensemble vs the oracle (weights restored to 1)
+    ens.t["weight"].fill_(1.0)
+    J = [torch.zeros((g, g, g), device="cuda", dtype=torch.float32) for _ in range(3)]
+    lb.boris_deposit_current(ens.handle, h, w.dt, *(j.data_ptr() for j in J))
+    torch.cuda.synchronize()
+    Jg = torch.stack(J).double().cpu().numpy()
+    pos = torch.stack([ens.t[k] for k in ("x", "y", "z")], 1).double().cpu().numpy()
+    mom = torch.stack([ens.t[k] for k in ("px", "py", "pz")], 1).double().cpu().numpy()
+    tq, tm = [t[0] for t in w.types], [t[1] for t in w.types]
+    Jr = oracle.deposit_current(pos, mom, np.ones(n), np.zeros(n, np.int16), tq, tm,
+                                w.light_velocity, w.dt, params)
+    m = tm[0]
+    gam = np.sqrt(1.0 + ((mom / (m * w.light_velocity)) ** 2).sum(1))[:, None]
+    vol = params[3] * params[4] * params[5]
+    contrib = (abs(tq[0]) * np.abs(mom / (m * gam)) / vol).sum(0)
+    err = np.abs(Jg - Jr).reshape(3, -1).max(1)
+    assert (err <= 1e-5 * contrib).all(), err / contrib
+    lb.boris_field_destroy(h)
+    ens.close()
+
+
+def test_full_size_fused_pic_step():
+    """boris_push_deposit at the PIC benchmark size (10^7 fp32, 64^3, sorted, the
+    configuration scripts/pic_cycle.py times): the state is bitwise the single-step grid
+    push's, J equals boris_deposit_current of the pushed state within the summation
+    bound, and the KE diagnostic counts every particle."""
+    h, params, comps = _grid64("fp32")
+    w = synth.config("C2", n=10_000_000)
+    n = w.n
+    d = w.generate(0, n, device="cuda")
+    a = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity, with_fields=False)
+    b = SoaEnsemble(n, lb.BORIS_FP32, w.types, w.light_velocity, with_fields=False)
+    for e in (a, b):
+        e.fill(d)
+        e.wrap()
+        lb.boris_ensemble_sort_by_cell(e.handle, h)
+    g = 64
+    Ja = [torch.zeros((g, g, g), device="cuda") for _ in range(3)]
+    Jb = [torch.zeros((g, g, g), device="cuda") for _ in range(3)]
+    diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+    lb.boris_push_deposit(a.handle, h, w.dt, *(j.data_ptr() for j in Ja), diag.data_ptr())
+    lb.boris_push(b.handle, h, w.dt, 1)
+    lb.boris_deposit_current(b.handle, h, w.dt, *(j.data_ptr() for j in Jb))
+    torch.cuda.synchronize()
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(a.t[k], b.t[k]), k
+    assert diag[1].item() == n
+    m, q = w.types[0][1], w.types[0][0]
+    mom = torch.stack([b.t[k] for k in ("px", "py", "pz")], 1).double()
+    gam = torch.sqrt(1.0 + ((mom / (m * w.light_velocity)) ** 2).sum(1, keepdim=True))
+    vol = params[3] * params[4] * params[5]
+    contrib = (abs(q) * (mom / (m * gam)).abs() / vol).sum(0).cpu().numpy()
+    err = (torch.stack(Ja).double() - torch.stack(Jb).double()).abs().reshape(3, -1).max(1)
+    assert (err.values.cpu().numpy() <= 1e-5 * contrib).all()
+    lb.boris_field_destroy(h)
+    a.close()
+    b.close()
+
+
 def test_sorted_push_equals_unsorted_push_bitwise():
     """The push of each particle is independent of order: sorted and unsorted
     ensembles give bit-identical particles (matched by id)."""
