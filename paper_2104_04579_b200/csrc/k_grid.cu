@@ -89,6 +89,12 @@ static PermPlan perm_plan(const SoaPtrs &s) {
 // contiguous 16 B vector stores: every written sector is written whole either way
 // (scalar stores at a 36 B lane stride took 3x the time of the traffic).
 constexpr int kPackTile = 256;
+#ifndef BORIS_UNPACK_VEC
+#define BORIS_UNPACK_VEC 1
+#endif
+#ifndef BORIS_UNPACK_NA
+#define BORIS_UNPACK_NA 0
+#endif
 
 template <typename FP>
 __global__ void __launch_bounds__(kPackTile)
@@ -365,7 +371,21 @@ __global__ void k_gather_bytes(const unsigned char *in, unsigned char *out, cons
 
 // Four particles per thread (i = base + k*256 + tid): 4 x RS independent record
 // loads in flight, every store warp-coalesced.
-template <typename FP>
+// A record read: __ldg by default; BORIS_UNPACK_NA (L1 no-allocate) measured worse
+// from random order (126 vs 112 B of DRAM read per particle, 270 vs 236 us at 1e7).
+__device__ __forceinline__ uint4 ld_record(const uint4 *p) {
+    uint4 v;
+#if BORIS_UNPACK_NA
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+#else
+    v = __ldg(p);
+#endif
+    return v;
+}
+
+template <typename FP, bool VEC = false>
 __global__ void __launch_bounds__(256)
     k_unpack_soa(const __grid_constant__ PermPlan p, const uint32_t *perm, int64_t n,
                  const FP *rec) {
@@ -385,10 +405,20 @@ __global__ void __launch_bounds__(256)
         for (int k = 0; k < U; ++k) {
             if (j[k] < 0) continue;
             const FP *r = rec + j[k] * p.rs;
+            if constexpr (VEC) {  // record of nf FP slots, a 16 B multiple, no type slot
+                constexpr int V = 16 / sizeof(FP);
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
-                if (a < p.nf) v[k][a] = __ldg(r + a);
-            if (p.type) t[k] = __ldg(reinterpret_cast<const W *>(r) + p.nf);
+                for (int h = 0; h < 8 / V; ++h)
+                    if (h * V < p.nf) {
+                        const uint4 u = ld_record(reinterpret_cast<const uint4 *>(r) + h);
+                        memcpy(&v[k][h * V], &u, 16);
+                    }
+            } else {
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+                    if (a < p.nf) v[k][a] = __ldg(r + a);
+                if (p.type) t[k] = __ldg(reinterpret_cast<const W *>(r) + p.nf);
+            }
         }
 #pragma unroll
         for (int k = 0; k < U; ++k) {
@@ -485,7 +515,10 @@ cudaError_t sort_by_cell(const EnsView &e, const GridArgs<FP> &g, int /*device*/
                 err = cudaGetLastError();
             }
             if (err == cudaSuccess) {
-                k_unpack_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(plan, v0, n, rec);
+                if (fused_pack && BORIS_UNPACK_VEC)
+                    k_unpack_soa<FP, true><<<grid1d((n + 3) / 4), 256, 0, st>>>(plan, v0, n, rec);
+                else
+                    k_unpack_soa<FP><<<grid1d((n + 3) / 4), 256, 0, st>>>(plan, v0, n, rec);
                 err = cudaGetLastError();
             }
         } else {
