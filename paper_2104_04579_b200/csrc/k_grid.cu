@@ -681,6 +681,9 @@ constexpr int kDepTile = 32 * kDepK;
 #ifndef BORIS_DEP_PREP
 #define BORIS_DEP_PREP 1
 #endif
+// MULTI / HAS_W compile-time: no per-tile default-value moves or predicated loads
+// for an absent weight array or type table.
+template <bool MULTI, bool HAS_W>
 __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
     k_deposit_runs(EnsView e, const __grid_constant__ GridArgs<float> g,
                    const __grid_constant__ DepCoefs<float> dc, const DepOut<float> o) {
@@ -689,7 +692,7 @@ __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
     const float *arr[7] = {(const float *)e.soa.x, (const float *)e.soa.y, (const float *)e.soa.z,
                            (const float *)e.soa.px, (const float *)e.soa.py,
                            (const float *)e.soa.pz, (const float *)e.soa.w};
-    const bool multi = dc.n_types > 1 && e.soa.type;
+    constexpr bool multi = MULTI;
     const int64_t stride = (int64_t)gridDim.x * kDepWarps * kDepTile;
     for (int64_t base = ((int64_t)blockIdx.x * kDepWarps + warp) * kDepTile; base < e.n;
          base += stride) {
@@ -703,8 +706,9 @@ __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
             for (int a = 0; a < 7; ++a)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const float4 v = arr[a] ? __ldg(reinterpret_cast<const float4 *>(arr[a] + i0) + h)
-                                            : make_float4(1.f, 1.f, 1.f, 1.f);
+                    const float4 v = (a < 6 || HAS_W)
+                                         ? __ldg(reinterpret_cast<const float4 *>(arr[a] + i0) + h)
+                                         : make_float4(1.f, 1.f, 1.f, 1.f);
                     rv[a][4 * h] = v.x; rv[a][4 * h + 1] = v.y;
                     rv[a][4 * h + 2] = v.z; rv[a][4 * h + 3] = v.w;
                 }
@@ -720,7 +724,7 @@ __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
                 const int64_t i = i0 + j;
 #pragma unroll
                 for (int a = 0; a < 7; ++a)
-                    rv[a][j] = (i < e.n) ? (arr[a] ? arr[a][i] : 1.f) : 0.f;
+                    rv[a][j] = (i < e.n) ? ((a < 6 || HAS_W) ? arr[a][i] : 1.f) : 0.f;
                 rty[j] = (multi && i < e.n) ? e.soa.type[i] : (int16_t)0;
             }
         }
@@ -851,7 +855,13 @@ static cudaError_t launch_deposit_kernel(const EnsView &e, const GridArgs<FP> &g
             const int64_t tiles = (e.n + kDepTile - 1) / kDepTile;
             const int64_t blocks = (tiles + kDepWarps - 1) / kDepWarps;
             const unsigned grid = (unsigned)stream_grid(blocks, 4, device);
-            k_deposit_runs<<<grid, kDepWarps * 32, 0, st>>>(e, g, dc, o);
+            const bool multi = dc.n_types > 1 && e.soa.type, w = e.soa.w != nullptr;
+            if (multi)
+                w ? k_deposit_runs<true, true><<<grid, kDepWarps * 32, 0, st>>>(e, g, dc, o)
+                  : k_deposit_runs<true, false><<<grid, kDepWarps * 32, 0, st>>>(e, g, dc, o);
+            else
+                w ? k_deposit_runs<false, true><<<grid, kDepWarps * 32, 0, st>>>(e, g, dc, o)
+                  : k_deposit_runs<false, false><<<grid, kDepWarps * 32, 0, st>>>(e, g, dc, o);
             return cudaGetLastError();
         }
     }
