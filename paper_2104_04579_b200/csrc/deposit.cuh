@@ -112,12 +112,16 @@ struct DepositRun {
         fl[0] = fl[1] = fl[2] = FP(0);
     }
 
-    // Atomics for the open cell (if any), then zero the sums.
+    // Atomics for the open cell (if any), then zero the sums (LAST: the run ends
+    // here and is reset before any reuse, so the sums are left as they are).
+    template <bool LAST = false>
     __device__ __forceinline__ void flush(const DepOut<FP> &o) {
         if (nb == kNoNode) return;
         red_cell(o, nb, acc);
+        if constexpr (!LAST) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+            for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = acc[q][2] = FP(0);
+        }
     }
 
     // One particle (state after the push: r^{n+1}, p^{n+1/2}, weight w).
@@ -211,7 +215,7 @@ struct DepositRun {
         uint32_t nbs[32];  // lane l's open cell (base node)
     };
 
-    // End of a warp tile (all 32 lanes), transposed: every lane stashes its 24 sums
+    // End of a warp tile (all 32 lanes; the run ends), transposed: every lane stashes its 24 sums
     // in shared memory, then lane t < 24 walks component t of the 32 lanes in lane
     // order and closes each run of equal open cells (contiguous when sorted) at its
     // last lane, where lanes 3q..3q+2 pass their components to lane 3q for one node
@@ -227,12 +231,9 @@ struct DepositRun {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                sm.red[(q * 3 + d) * RS + lane] = acc[q][d];
-                acc[q][d] = FP(0);
-            }
+            for (int d = 0; d < 3; ++d) sm.red[(q * 3 + d) * RS + lane] = acc[q][d];
         sm.nbs[lane] = nb;
-        nb = kNoNode;
+        nb = kNoNode;  // the run ends: reset() before reuse (the sums are left)
         __syncwarp();
         const int t = lane < 24 ? lane : 23;  // lanes 24..31 shadow lane 23 (no atomics)
         const int q = t / 3, d = t - 3 * (t / 3);

@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
             run.merge_flush(o, s_merge[warp], lane);
         } else {
             run.warp_merge(lane);
-            run.flush(o);
+            run.flush<true>(o);
         }
         __syncwarp();
     }

@@ -263,7 +263,7 @@ template cudaError_t launch_stream_soa_grid<double>(const EnsView &, const GridA
 #ifndef BORIS_PD_MINB
 #define BORIS_PD_MINB 2
 #endif
-template <typename FP, bool MULTI, bool DIAG>
+template <typename FP, bool MULTI, bool DIAG, bool HAS_W>
 __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
     k_push_deposit_soa(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
                        const __grid_constant__ KCoefs<FP, MULTI> co,
@@ -301,8 +301,9 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             pz.load_state(PZ + i0);
             int ty[V];
             if (MULTI) load_types<V>(s.type + i0, ty);
-            if (W) w.load_field(W + i0);
-            else {
+            if constexpr (HAS_W) {
+                w.load_field(W + i0);
+            } else {
 #pragma unroll
                 for (int j = 0; j < V; ++j) w.v[j] = FP(1);
             }
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             run.merge_flush(o, s_merge[threadIdx.x >> 5], lane);
         } else {
             run.warp_merge(lane);
-            run.flush(o);
+            run.flush<true>(o);
         }
     }
     // ragged tail (n mod V particles): push then deposit directly
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
         FP ux, uy, uz, gam, Ex, Ey, Ez, Bx, By, Bz;
         FP x = X[i], y = Y[i], z = Z[i], px = PX[i], py = PY[i], pz = PZ[i];
-        const FP w = W ? W[i] : FP(1);
+        const FP w = HAS_W ? W[i] : FP(1);
         grid_gather<FP>(g, x, y, z, Ex, Ey, Ez, Bx, By, Bz);
         push_one<FP>(x, y, z, px, py, pz, gam, Ex, Ey, Ez, Bx, By, Bz, tc, ux, uy, uz);
         X[i] = x; Y[i] = y; Z[i] = z; PX[i] = px; PY[i] = py; PZ[i] = pz; G[i] = gam;
@@ -389,8 +390,12 @@ static cudaError_t dispatch_push_deposit(const EnsView &e, const GridArgs<FP> &g
     const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, BORIS_PD_MINB, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    k_push_deposit_soa<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
-        e.soa, g, kcoefs<MULTI>(co), dc, o, n_groups, e.n, diag ? diag->partials : nullptr);
+    if (e.soa.w)
+        k_push_deposit_soa<FP, MULTI, DIAG, true><<<(unsigned)grid, kStreamThreads, 0, st>>>(
+            e.soa, g, kcoefs<MULTI>(co), dc, o, n_groups, e.n, diag ? diag->partials : nullptr);
+    else
+        k_push_deposit_soa<FP, MULTI, DIAG, false><<<(unsigned)grid, kStreamThreads, 0, st>>>(
+            e.soa, g, kcoefs<MULTI>(co), dc, o, n_groups, e.n, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
     return cudaGetLastError();
 }
