@@ -11,6 +11,9 @@
 
 namespace boris {
 
+#ifndef BORIS_GRID_AXIS_FAST
+#define BORIS_GRID_AXIS_FAST 0
+#endif
 constexpr int kGridRecord = 12;  // FP per x-pair record: [E B](i) [E B](i+1)
 
 template <typename FP>
@@ -31,10 +34,18 @@ __device__ __forceinline__ void grid_axis(FP x, FP org, FP inv_h, FP nf, FP inv_
     const FP xi = b_mul(b_add(x, -org), inv_h);
     const FP fl = floor(xi);
     f = b_add(xi, -fl);  // exact, in [0, 1)
-    const FP w = b_fma(-nf, floor(b_mul(fl, inv_nf)), fl);  // fl mod n, up to +-1 rounding
-    int i = (int)w;
-    if (i >= n) i -= n;
-    if (i < 0) i += n;
+    int i;
+#if BORIS_GRID_AXIS_FAST
+    if (fl >= FP(0) && fl < nf) {  // inside the periodic box: no wrap needed
+        i = (int)fl;
+    } else
+#endif
+    {
+        const FP w = b_fma(-nf, floor(b_mul(fl, inv_nf)), fl);  // fl mod n, up to +-1 rounding
+        i = (int)w;
+        if (i >= n) i -= n;
+        if (i < 0) i += n;
+    }
     i0 = i;
     i1 = (i + 1 == n) ? 0 : i + 1;
 }
