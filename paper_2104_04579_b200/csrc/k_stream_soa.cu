@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             FP ex[V], ey[V], ez[V], bx[V], by[V], bz[V];
 #pragma unroll
             for (int j = 0; j < V; ++j)
-                grid_gather<FP>(g, x.v[j], y.v[j], z.v[j], ex[j], ey[j], ez[j], bx[j], by[j],
+                grid_gather<FP, true>(g, x.v[j], y.v[j], z.v[j], ex[j], ey[j], ez[j], bx[j],
+                                      by[j],
                                 bz[j]);
 #pragma unroll
             for (int j = 0; j < V; ++j) {
