@@ -166,6 +166,16 @@ __global__ void __launch_bounds__(kRsThreads)
     const uint32_t mask = (uint32_t)bins - 1u;
     const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
     const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+    // warp-aggregated: one shared atomic per distinct digit in the warp (sorted input
+    // puts a whole warp in one bin, where per-lane atomics serialise)
+    auto count_digit = [&](int d) {
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d < bins && __popc(peers & lt) == 0) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+    };
+    // later passes: all rounds' key loads first, then the warp-synchronous counting
+    // (pass 1 hist 33 -> 24 us at 1e7); pass 0 counts per round (measured faster with
+    // its position loads and record stores)
+    int dg[kRsItems];
 #pragma unroll
     for (int r = 0; r < kRsItems; ++r) {
         const int64_t i = t0 + r * kRsThreads + threadIdx.x;
@@ -205,10 +215,12 @@ __global__ void __launch_bounds__(kRsThreads)
             }
             d = (int)((key >> shift) & mask);
         }
-        // warp-aggregated: one shared atomic per distinct digit in the warp (sorted
-        // input puts a whole warp in one bin, where per-lane atomics serialise)
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        if (d < bins && __popc(peers & lt) == 0) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+        dg[r] = d;
+        if constexpr (KEYS) count_digit(d);  // pass 0: count as the keys arrive
+    }
+    if constexpr (!KEYS) {
+#pragma unroll
+        for (int r = 0; r < kRsItems; ++r) count_digit(dg[r]);
     }
     __syncthreads();
     for (int b = threadIdx.x; b < bins; b += kRsThreads)
