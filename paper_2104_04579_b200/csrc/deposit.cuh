@@ -250,6 +250,13 @@ struct DepositRun {
                 const double2 w = reinterpret_cast<const double2 *>(row)[l0 / 2];
                 v[0] = w.x; v[1] = w.y;
             }
+            if (((tails >> l0) & ((1u << VW) - 1u)) == 0) {  // no run ends here (uniform)
+                FP gsum = v[0];
+#pragma unroll
+                for (int k = 1; k < VW; ++k) gsum = b_add(gsum, v[k]);
+                run = b_add(run, gsum);
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < VW; ++k) {
                 run = b_add(run, v[k]);
