@@ -15,6 +15,16 @@
 #include "boris_internal.h"
 #include "tma.cuh"
 
+// fp32: 8 stages (one CTA per SM, 122 KB of tiles in flight) measured best: 14.9 ps at
+// 1e8 vs 15.3 with 4 stages x 3 CTAs (6, 10, 12, 14 stages: 15.0-15.7,
+// profiles/r02/exp_aos_stages.jsonl); fp64 3 stages (2-14 tried).
+#ifndef BORIS_AOS_STAGES32
+#define BORIS_AOS_STAGES32 8
+#endif
+#ifndef BORIS_AOS_STAGES64
+#define BORIS_AOS_STAGES64 3
+#endif
+
 namespace boris {
 
 namespace {
@@ -25,7 +35,7 @@ struct AosGeom {
                                               : BORIS_AOS_RECORD_BYTES_FP64;
     static constexpr int FB = 6 * (int)sizeof(FP);
     static constexpr int TP = kAosThreads;           // particles per tile
-    static constexpr int STAGES = sizeof(FP) == 4 ? 4 : 3;
+    static constexpr int STAGES = sizeof(FP) == 4 ? BORIS_AOS_STAGES32 : BORIS_AOS_STAGES64;
     static constexpr int TILE_R = TP * RB;           // 9216 / 18432 B
     static constexpr int TILE_F = TP * FB;           // 6144 / 12288 B
     static constexpr int SMEM = STAGES * (TILE_R + TILE_F) + STAGES * 8;
