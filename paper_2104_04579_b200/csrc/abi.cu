@@ -172,7 +172,9 @@ boris_status check_device(int device) {
 }
 
 boris_status alloc_scratch(boris_ensemble *e) {
-    e->partials_cap = (int64_t)sm_count(e->device) * 64;
+    // one (KE, count) pair per block of the largest diagnostic grid (stream_grid at
+    // 8 blocks of 256 per SM)
+    e->partials_cap = (int64_t)sm_count(e->device) * 8 * kStreamWaves;
     CUDA_TRY(cudaMalloc(&e->partials, (size_t)e->partials_cap * 2 * sizeof(double)),
              "cudaMalloc(diag partials)");
     CUDA_TRY(cudaMalloc(&e->d_bad, sizeof(unsigned long long)), "cudaMalloc(type check)");

@@ -79,7 +79,11 @@ cudaError_t scratch_alloc(void **ptr, size_t bytes, cudaStream_t st);
 void scratch_free(void *ptr, cudaStream_t st);
 
 // Grid of a grid-stride launch: min(work blocks, SMs x resident blocks x waves).
-int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device);
+#ifndef BORIS_STREAM_WAVES
+#define BORIS_STREAM_WAVES 64
+#endif
+constexpr int kStreamWaves = BORIS_STREAM_WAVES;
+int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device, int waves = 4);
 // Grid of an ALU-bound grid-stride launch: min(work blocks, SMs x the kernel's
 // resident blocks per SM) -- one wave, equal work per block.
 int64_t resident_grid(const void *kernel, int threads, int64_t work_blocks, int device);

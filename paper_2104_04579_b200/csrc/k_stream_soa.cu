@@ -483,14 +483,14 @@ static cudaError_t dispatch_soa(const EnsView &e, const FieldSoaPtrs &f, const C
     if (vec) {
         const int64_t n_groups = e.n / V;
         const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
-        grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+        grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device, kStreamWaves);
         if (DIAG && grid > diag->cap) grid = diag->cap;
         k_stream_soa_vec<FP, MULTI, DIAG>
             <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, kcoefs<MULTI>(co), n_groups, e.n,
                                                         partials);
     } else {
         const int64_t blocks = (e.n + kStreamThreads - 1) / kStreamThreads;
-        grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+        grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device, kStreamWaves);
         if (DIAG && grid > diag->cap) grid = diag->cap;
         k_stream_soa_scalar<FP, MULTI, DIAG>
             <<<(unsigned)grid, kStreamThreads, 0, st>>>(e.soa, f, kcoefs<MULTI>(co), e.n, partials);

@@ -58,10 +58,15 @@ void scratch_free(void *ptr, cudaStream_t st) {
     if (ptr) cudaFreeAsync(ptr, st);
 }
 
-int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device) {
-    // Grid-stride kernels: enough blocks for every SM to hold `blocks_per_sm`
-    // resident blocks, times a few waves so the tail wave is short.
-    const int64_t cap = (int64_t)sm_count(device) * blocks_per_sm * 4;
+int64_t stream_grid(int64_t work_blocks, int blocks_per_sm, int device, int waves) {
+    // Grid-stride kernels: up to `waves` waves of `blocks_per_sm` resident blocks per SM.
+    // The pure HBM streams (k_stream_soa_*) take kStreamWaves = 64: many short-lived
+    // blocks beat few looping ones there, fresh blocks issuing their loads while retiring
+    // blocks store (C2 fp32 SoA at 1e8: 4 waves 11.66 ps, 16: 11.36, 64: 11.12 = 6.83
+    // TB/s; C5 bench 0.97 -> 1.00 of copy).  The gather / deposition kernels keep 4
+    // (64 measured slower: grid push 11.4 -> 11.9 ps, PIC 25.3 -> 28.7,
+    // profiles/r02/exp_stream_waves.jsonl).
+    const int64_t cap = (int64_t)sm_count(device) * blocks_per_sm * waves;
     return work_blocks < cap ? work_blocks : cap;
 }
 
@@ -120,7 +125,7 @@ template <typename FP>
 cudaError_t launch_kinetic_energy(const EnsView &e, const Coefs<FP> &co, bool multi,
                                   DiagOut *diag, int device, cudaStream_t st) {
     const int64_t blocks = (e.n + kStreamThreads - 1) / kStreamThreads;
-    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
+    int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device, kStreamWaves);
     if (grid > diag->cap) grid = diag->cap;
     const bool soa = e.layout == BORIS_LAYOUT_SOA;
     if (soa && multi)
