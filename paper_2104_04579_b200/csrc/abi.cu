@@ -375,7 +375,18 @@ cudaError_t push_view(const boris_ensemble *e, const EnsView &v, const boris_fie
         }
         return cudaSuccess;
     }
-    const AnalyticArgs<FP> fa = make_analytic<FP>(f, t0, dt);
+    AnalyticArgs<FP> fa = make_analytic<FP>(f, t0, dt);
+    if (f->kind == FK_MDIPOLE && !e->multi()) {  // k_fused kMdFold scaled variables
+        const double q = e->types[0].charge, mc = e->types[0].mass * e->c;
+        const double alpha = q * dt / (2.0 * mc);  // eq. 9-10, 13 with u = p/(m c)
+        fa.mdf_k = f->kd;
+        fa.mdf_ik = 1.0 / f->kd;
+        fa.mdf_kick = alpha * 2.0 * f->A0;
+        fa.mdf_rot = alpha * -2.0 * f->A0;
+        fa.mdf_uin = (FP)(1.0 / mc);
+        fa.mdf_uout = (FP)mc;
+        fa.mdf_cr = (FP)(f->kd * e->c * dt);  // eq. 7: dX = k c dt u / gamma
+    }
     if (f->kind == FK_GRID && n_steps == 1 && v.layout == BORIS_LAYOUT_SOA &&
         pusher == PUSHER_BORIS) {  // the PIC single step: 128-bit streaming + gather
         const cudaError_t err =

@@ -49,6 +49,12 @@ struct AnalyticArgs {
     FP A0k2;         // 2 A0 k
     FP mA02;         // -2 A0
     double w0t0, w0dt;
+    // single-type Boris m-dipole (k_fused kMdFold; push_view fills these): the step runs
+    // in the scaled variables X = k r, u = p/(m c), so that xi^2 = |X|^2 and
+    // gamma^2 = 1 + |u|^2 (no k^2, kappa^2 factors in the loop)
+    double mdf_k, mdf_ik;        // k, 1/k
+    double mdf_kick, mdf_rot;    // (q dt / 2 m c) 2 A0, (q dt / 2 m c) (-2 A0)
+    FP mdf_uin, mdf_uout, mdf_cr;  // 1/(m c), m c, k c dt
     // grid (FK_GRID): CIC gather of packed node records (grid.cuh)
     GridArgs<FP> grid;
     // uniform / plane wave with E || y^, B || z^ (k^ = x^): the k_fused YZ

@@ -11,6 +11,8 @@
 // otherwise idle FP64 pipe) and evaluate the plane-wave phase in fp64 with an
 // exact 2-pi range reduction before the fp32 cosine (SURVEY §8(c) "GPU<->oracle,
 // fp32": this quadruples the margin under the 1e-5 bar at C4).
+#include <type_traits>
+
 #include "boris_internal.h"
 
 namespace boris {
@@ -52,21 +54,26 @@ __device__ __forceinline__ double cos_small(double x) { return cos(x); }
 // Taylor coefficients generated at compile time from their defining series:
 //   j0 = sum (-1)^n xi^{2n}/(2n+1)!,  j1/xi = sum (-1)^n 2(n+1) xi^{2n}/(2n+3)!,
 //   g2 = sum_{n>=1} (-1)^n [6(n+1)/(2n+3)! - 1/(2n+1)!] xi^{2n-2}.
-struct MdSeries {
-    double j0[10], j1x[10], g2[10];
-};
+// The Horner chains below take them as template constants (FFMA immediates in the
+// fp32 SASS: no constant-bank loads, conversions or registers held for them).
 constexpr double fact(int k) { return k <= 1 ? 1.0 : k * fact(k - 1); }
-constexpr MdSeries make_md_series() {
-    MdSeries s{};
-    for (int n = 0; n < 10; ++n) {
-        const double sg = (n % 2 == 0) ? 1.0 : -1.0;
-        s.j0[n] = sg / fact(2 * n + 1);
-        s.j1x[n] = sg * 2.0 * (n + 1) / fact(2 * n + 3);
-        s.g2[n] = sg * (6.0 * (n + 1) / fact(2 * n + 3) - 1.0 / fact(2 * n + 1));  // used n >= 1
-    }
-    return s;
+constexpr double md_sign(int n) { return (n % 2 == 0) ? 1.0 : -1.0; }
+constexpr double md_j0c(int n) { return md_sign(n) / fact(2 * n + 1); }
+constexpr double md_j1xc(int n) { return md_sign(n) * 2.0 * (n + 1) / fact(2 * n + 3); }
+constexpr double md_g2c(int n) {  // used for n >= 1
+    return md_sign(n) * (6.0 * (n + 1) / fact(2 * n + 3) - 1.0 / fact(2 * n + 1));
 }
-__constant__ MdSeries c_md = make_md_series();
+// sum_{n=N}^{T-1} c_n x2^{n-N} by Horner from the top term (WHICH: 0 j0, 1 j1/xi, 2 g2)
+template <typename FP, int WHICH, int N, int T>
+struct MdHorner {
+    static __device__ __forceinline__ FP eval(FP x2) {
+        constexpr FP c = FP(WHICH == 0 ? md_j0c(N) : WHICH == 1 ? md_j1xc(N) : md_g2c(N));
+        if constexpr (N == T - 1)
+            return c;
+        else
+            return MdHorner<FP, WHICH, N + 1, T>::eval(x2) * x2 + c;
+    }
+};
 
 template <typename FP>
 struct MdBranch;
@@ -95,48 +102,40 @@ __device__ __forceinline__ double md_radius(double r2) { return __dsqrt_rn(r2); 
 
 // Closed-form branch of the radial functions (eq. 15, reading c11) from s = sin xi,
 // c = cos xi and i = 1/xi, factored so that each product is formed once:
+//   P  = i (s i) - c i
 //   g1 = f1/xi   = i^2 (s i - c)
-//   g2 = f2/xi^2 = i^3 (3 (i (s i) - c i) - s)
-//   f3           = i (s + c i - (s i) i)
+//   g2 = f2/xi^2 = i^3 (3 P - s)
+//   f3           = i (s - P)
 // (f1 = s/xi^2 - c/xi, f2 = (3/xi^3 - 1/xi) s - 3c/xi^2, f3 = (1/xi - 1/xi^3) s + c/xi^2).
 template <typename FP>
 __device__ __forceinline__ void md_closed(FP sn, FP cs, FP ix, FP &g1, FP &g2, FP &f3) {
     const FP a = b_mul(sn, ix), b = b_mul(cs, ix), i2 = b_mul(ix, ix);
+    const FP P = b_fma(ix, a, -b);
     g1 = b_mul(i2, b_add(a, -cs));
-    g2 = b_mul(b_mul(i2, ix), b_fma(FP(3), b_fma(ix, a, -b), -sn));
-    f3 = b_mul(ix, b_add(sn, b_fma(-a, ix, b)));
+    g2 = b_mul(b_mul(i2, ix), b_fma(FP(3), P, -sn));
+    f3 = b_mul(ix, b_add(sn, -P));
+}
+
+// Taylor branch (reading c13) from xi^2
+template <typename FP>
+__device__ __forceinline__ void md_taylor_series(FP x2, FP &g1, FP &g2, FP &f3) {
+    constexpr int T = MdBranch<FP>::terms;
+    const FP j0 = MdHorner<FP, 0, 0, T>::eval(x2);
+    const FP j1x = MdHorner<FP, 1, 0, T>::eval(x2);
+    g1 = j1x;
+    g2 = MdHorner<FP, 2, 1, T>::eval(x2);
+    f3 = j0 - j1x;
 }
 
 template <typename FP>
 __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
     if (xi < MdBranch<FP>::xi_star) {
-        const FP x2 = xi * xi;
-        constexpr int T = MdBranch<FP>::terms;
-        FP j0 = FP(c_md.j0[T - 1]), j1x = FP(c_md.j1x[T - 1]), s2 = FP(c_md.g2[T - 1]);
-#pragma unroll
-        for (int n = T - 2; n >= 0; --n) {
-            j0 = j0 * x2 + FP(c_md.j0[n]);
-            j1x = j1x * x2 + FP(c_md.j1x[n]);
-        }
-#pragma unroll
-        for (int n = T - 2; n >= 1; --n) s2 = s2 * x2 + FP(c_md.g2[n]);
-        g1 = j1x;
-        g2 = s2;
-        f3 = j0 - j1x;
+        md_taylor_series<FP>(xi * xi, g1, g2, f3);
     } else {
         FP sn, cs, ix;
         if constexpr (sizeof(FP) == 4) {
-#ifdef BORIS_PRECISE_MATH
             sincosf(xi, &sn, &cs);
             ix = 1.0f / xi;
-#else
-            // fp32 Cody-Waite reduction to [-pi, pi], then MUFU sin/cos (abs error
-            // ~2^-21, the fp32 rounding of xi itself) and rcp.approx
-            const float q = rintf(xi * 0.15915494f);
-            const float r = __fmaf_rn(-q, -1.7484555e-07f, __fmaf_rn(-q, 6.2831855f, xi));
-            __sincosf(r, &sn, &cs);
-            ix = b_rcpx(xi);
-#endif
         } else {
             sincos(xi, &sn, &cs);
             ix = __drcp_rn(xi);  // == 1.0 / xi (both correctly rounded), no division
@@ -145,13 +144,32 @@ __device__ __forceinline__ void md_radial(FP xi, FP &g1, FP &g2, FP &f3) {
     }
 }
 
-// The radial functions from r^2 = |r|^2 (both callers: the fused step and the branch
-// grouping).  fp32 (default math) works with xi^2 = k^2 r^2: the Taylor branch is a
+// The radial functions from xi^2 (fp32 / fp64 default math): the Taylor branch is a
 // series in xi^2 (no square root), and the closed form takes 1/xi = rsqrt(xi^2) from
-// one MUFU rsqrt and xi = xi^2 / xi -- one MUFU fewer than R = sqrt(r^2), xi = k R,
-// 1/xi = rcp(xi); the branch test xi < 1.5 becomes xi^2 < 2.25 (reading c13).  fp64
-// likewise with the double rsqrt (xi^2 < 1); BORIS_PRECISE_MATH uses R = sqrt(r^2),
-// xi = k R with correctly rounded square root and reciprocal.
+// one MUFU rsqrt and xi = xi^2 / xi; the branch test xi < xi* becomes xi^2 < xi*^2
+// (reading c13).  fp32 sin and cos of xi straight from the MUFU (sin.approx /
+// cos.approx: absolute error 2^-21.4 on [-pi, pi], growing with the 2^-23 relative
+// rounding of the argument's revolutions beyond, ~2^-21 at the sphere's xi = 3.8);
+// fp64 with the double rsqrt (1 ulp) and sincos.
+template <typename FP>
+__device__ __forceinline__ void md_radial_x2(FP x2, FP &g1, FP &g2, FP &f3) {
+    if (x2 < MdBranch<FP>::xi_star * MdBranch<FP>::xi_star) {
+        md_taylor_series<FP>(x2, g1, g2, f3);
+    } else {
+        FP sn, cs;
+        const FP ix = b_rsqrt(x2), xi = b_mul(x2, ix);
+        if constexpr (sizeof(FP) == 4)
+            __sincosf(xi, &sn, &cs);
+        else
+            sincos(xi, &sn, &cs);
+        md_closed<FP>(sn, cs, ix, g1, g2, f3);
+    }
+}
+
+// The radial functions from r^2 = |r|^2 (field evaluation, the multi-type and
+// alternative-pusher fused steps, the branch grouping): xi^2 = k^2 r^2 as above;
+// BORIS_PRECISE_MATH uses R = sqrt(r^2), xi = k R with correctly rounded square root
+// and reciprocal.
 template <typename FP>
 __device__ __forceinline__ bool md_taylor(const AnalyticArgs<FP> &fa, FP r2) {
 #ifndef BORIS_PRECISE_MATH
@@ -164,58 +182,10 @@ template <typename FP>
 __device__ __forceinline__ void md_radial_r2(const AnalyticArgs<FP> &fa, FP r2, FP &g1, FP &g2,
                                              FP &f3) {
 #ifndef BORIS_PRECISE_MATH
-    if constexpr (sizeof(FP) == 4) {
-        const float x2 = b_mul(fa.k2, r2);
-        if (x2 < MdBranch<float>::xi_star * MdBranch<float>::xi_star) {
-            constexpr int T = MdBranch<float>::terms;
-            float j0 = float(c_md.j0[T - 1]), j1x = float(c_md.j1x[T - 1]),
-                  s2 = float(c_md.g2[T - 1]);
-#pragma unroll
-            for (int n = T - 2; n >= 0; --n) {
-                j0 = j0 * x2 + float(c_md.j0[n]);
-                j1x = j1x * x2 + float(c_md.j1x[n]);
-            }
-#pragma unroll
-            for (int n = T - 2; n >= 1; --n) s2 = s2 * x2 + float(c_md.g2[n]);
-            g1 = j1x;
-            g2 = s2;
-            f3 = j0 - j1x;
-        } else {
-            const float ix = b_rsqrt(x2), xi = b_mul(x2, ix);
-            const float q = rintf(xi * 0.15915494f);
-            const float r = __fmaf_rn(-q, -1.7484555e-07f, __fmaf_rn(-q, 6.2831855f, xi));
-            float sn, cs;
-            __sincosf(r, &sn, &cs);
-            md_closed<float>(sn, cs, ix, g1, g2, f3);
-        }
-        return;
-    } else {
-        // fp64: the same from xi^2, with the double rsqrt (1 ulp) in place of the
-        // correctly rounded sqrt and reciprocal (two long software sequences)
-        const double x2 = b_mul(fa.k2, r2);
-        if (x2 < MdBranch<double>::xi_star * MdBranch<double>::xi_star) {
-            constexpr int T = MdBranch<double>::terms;
-            double j0 = c_md.j0[T - 1], j1x = c_md.j1x[T - 1], s2 = c_md.g2[T - 1];
-#pragma unroll
-            for (int n = T - 2; n >= 0; --n) {
-                j0 = j0 * x2 + c_md.j0[n];
-                j1x = j1x * x2 + c_md.j1x[n];
-            }
-#pragma unroll
-            for (int n = T - 2; n >= 1; --n) s2 = s2 * x2 + c_md.g2[n];
-            g1 = j1x;
-            g2 = s2;
-            f3 = j0 - j1x;
-        } else {
-            const double ix = rsqrt(x2), xi = b_mul(x2, ix);
-            double sn, cs;
-            sincos(xi, &sn, &cs);
-            md_closed<double>(sn, cs, ix, g1, g2, f3);
-        }
-        return;
-    }
-#endif
+    md_radial_x2<FP>(b_mul(fa.k2, r2), g1, g2, f3);
+#else
     md_radial<FP>(b_mul(fa.k, md_radius(r2)), g1, g2, f3);
+#endif
 }
 
 template <typename FP, int FIELD>
@@ -428,22 +398,25 @@ __global__ void __launch_bounds__(kFusedThreads)
     constexpr int kFlush = kFlushOf<FP>;
     constexpr bool kMerged = kMergedRsqrt<FP, FIELD>;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
-    __shared__ FP s_sin[FIELD == FK_MDIPOLE ? kTimeTab : 1];
-    __shared__ FP s_cos[FIELD == FK_MDIPOLE ? kTimeTab : 1];
+    // m-dipole time table: .x the sin(w0 t_j) factor, .y the cos(w0 t_j) factor
+    using FP2 = typename std::conditional<sizeof(FP) == 4, float2, double2>::type;
+    __shared__ FP2 s_tab[FIELD == FK_MDIPOLE ? kTimeTab : 1];
     if (MULTI) load_type_table(co, s_t);
-    // single-type Boris m-dipole: the type's half-kick and rotation factors are folded
-    // into the time tables (kMdFold: t and the kick come straight from the field's
-    // scalar factors, no E, B vectors are formed)
+    // single-type Boris m-dipole (kMdFold): the step runs in X = k r, u = p/(m c)
+    // (AnalyticArgs mdf_*), with the type's half-kick and rotation factors folded into
+    // the time table (t and the kick come straight from the field's scalar factors, no
+    // E, B vectors are formed)
     constexpr bool kMdFold = FIELD == FK_MDIPOLE && !MULTI && PUSHER == PUSHER_BORIS;
     if constexpr (FIELD == FK_MDIPOLE) {
         for (int j = threadIdx.x; j < n_steps; j += kFusedThreads) {
             double sn, cs;
             sincos(fa.w0t0 + (double)j * fa.w0dt, &sn, &cs);  // t_j = t0 + j dt (c5)
-            s_sin[j] = b_mul(fa.mA02, (FP)sn);   // -2 A0 sin(w t_j)
-            s_cos[j] = b_mul(fa.A0k2, (FP)cs);   // 2 A0 k cos(w t_j)
             if (kMdFold) {
-                s_sin[j] = b_mul(co.t[0].alpha, s_sin[j]);  // alpha (-2 A0 sin)
-                s_cos[j] = b_mul(co.t[0].aE, s_cos[j]);     // aE (2 A0 k cos)
+                s_tab[j].x = (FP)(fa.mdf_rot * sn);   // (q dt / 2mc) (-2 A0 sin(w t_j))
+                s_tab[j].y = (FP)(fa.mdf_kick * cs);  // (q dt / 2mc) 2 A0 cos(w t_j)
+            } else {
+                s_tab[j].x = b_mul(fa.mA02, (FP)sn);  // -2 A0 sin(w t_j)
+                s_tab[j].y = b_mul(fa.A0k2, (FP)cs);  // 2 A0 k cos(w t_j)
             }
         }
         __syncthreads();
@@ -457,7 +430,14 @@ __global__ void __launch_bounds__(kFusedThreads)
         Particle<FP, LAYOUT>::load(e, i, xa, ya, za, px, py, pz, w, ty);
         if (!MULTI) ty = 0;
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
-        FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
+        const FP uin = kMdFold ? fa.mdf_uin : tc.S;
+        FP ux = b_mul(px, uin), uy = b_mul(py, uin), uz = b_mul(pz, uin);
+        if constexpr (kMdFold) {
+            xa *= fa.mdf_k;
+            ya *= fa.mdf_k;
+            za *= fa.mdf_k;
+        }
+        const FP crf = kMdFold ? fa.mdf_cr : tc.cr;
         FP gam = FP(1);
         // uniform / plane wave: E = c e, B = c b with fixed e, b -> per-particle aE e, alpha b
         FP ae[3], ab[3];
@@ -544,33 +524,37 @@ __global__ void __launch_bounds__(kFusedThreads)
 #endif
                     inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
                 } else if constexpr (kMdFold) {  // eq. 14 (c9, c10, c13), factors folded
-                    // E = ce g1 (-y, x, 0), B = sb (k^2 g2 z r + f3 z^); the kick is
-                    // aE E = e (-y, x, 0) with e = (aE ce) g1, and the rotation vector
-                    // t = alpha B / gamma_n = a r + b z^ with a = (alpha sb / gamma_n) k^2 g2 z,
-                    // b = (alpha sb / gamma_n) f3 (eq. 9-13; E_z = 0 exactly)
+                    // In X = k r: E = 2 A0 cos(w t) g1 (-Y, X, 0), B = -2 A0 sin(w t)
+                    // (g2 Z X + f3 z^), xi^2 = |X|^2.  The kick is (q dt/2mc) E =
+                    // e (-Y, X, 0) with e = tab.y g1, and the rotation vector
+                    // t = (q dt/2mc) B / gamma_n = a X + b z^ with a = (tab.x / gamma_n) g2 Z,
+                    // b = (tab.x / gamma_n) f3 (eq. 9-13; E_z = 0 exactly)
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
                     FP g1, g2, f3;
-                    md_radial_r2<FP>(fa, b_norm2(x, y, z), g1, g2, f3);
-                    const FP e = b_mul(s_cos[s0 + j], g1);
+                    md_radial_x2<FP>(b_norm2(x, y, z), g1, g2, f3);
+                    const FP2 tab = s_tab[s0 + j];
+                    const FP e = b_mul(tab.y, g1);
                     ux = b_fma(-e, y, ux);
                     uy = b_fma(e, x, uy);
-                    const FP tsb = b_mul(s_sin[s0 + j], b_rsqrt(b_fma(tc.kappa2,
-                                                                      b_norm2(ux, uy, uz), FP(1))));
-                    const FP al = b_mul(tsb, b_mul(b_mul(fa.k2, g2), z));
+                    // 1/gamma_n = rsqrt(1 + |u|^2)  (eq. 5 with kappa = 1)
+                    const FP tsb = b_mul(tab.x, b_rsqrt(b_fma(ux, ux, b_fma(uy, uy,
+                                                                       b_fma(uz, uz, FP(1))))));
+                    const FP al = b_mul(tsb, b_mul(g2, z));
                     boris_rotate<FP>(ux, uy, uz, b_mul(al, x), b_mul(al, y),
                                      b_fma(al, z, b_mul(tsb, f3)));
                     ux = b_fma(-e, y, ux);
                     uy = b_fma(e, x, uy);
-                    // gamma^{n+1/2} is stored once after the loop (same operations)
-                    inv_g = b_rsqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
+                    // gamma^{n+1/2} is stored once after the loop
+                    inv_g = b_rsqrt(b_fma(ux, ux, b_fma(uy, uy, b_fma(uz, uz, FP(1)))));
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
                     FP g1, g2, f3;
                     md_radial_r2<FP>(fa, b_norm2(x, y, z), g1, g2, f3);
                     // per-block tables hold the amplitudes (same roundings as in the step)
-                    const FP ce = b_mul(s_cos[s0 + j], g1);  // 2 A0 k cos(w t) f1/xi
-                    const FP sb = s_sin[s0 + j];             // -2 A0 sin(w t)
+                    const FP2 tab = s_tab[s0 + j];
+                    const FP ce = b_mul(tab.y, g1);  // 2 A0 k cos(w t) f1/xi
+                    const FP sb = tab.x;             // -2 A0 sin(w t)
                     const FP k2g2 = b_mul(fa.k2, g2);               // f2/R^2
                     Ex = -b_mul(ce, y);
                     Ey = b_mul(ce, x);
@@ -587,7 +571,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                                                             tc, gam);
                 }
                 // a10 (eq. 7): displacement accumulated in the window
-                const FP ct = b_mul(tc.cr, inv_g);
+                const FP ct = b_mul(crf, inv_g);
                 dx = b_fma(ct, ux, dx);
                 dy = b_fma(ct, uy, dy);
                 dz = b_fma(ct, uz, dz);
@@ -606,7 +590,15 @@ __global__ void __launch_bounds__(kFusedThreads)
             ya = __dadd_rn(ya, (double)dy);
             za = __dadd_rn(za, (double)dz);
         }
-        const double x = xa, y = ya, z = za;
+        double x = xa, y = ya, z = za;
+        if constexpr (kMdFold) {  // back from X = k r, u = p/(m c); then u = S p as elsewhere
+            x *= fa.mdf_ik;
+            y *= fa.mdf_ik;
+            z *= fa.mdf_ik;
+            ux = b_mul(b_mul(ux, fa.mdf_uout), tc.S);
+            uy = b_mul(b_mul(uy, fa.mdf_uout), tc.S);
+            uz = b_mul(b_mul(uz, fa.mdf_uout), tc.S);
+        }
         if (n_steps == 0) gam = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
         else if (kMdFold) boris_gamma<FP>(ux, uy, uz, tc.kappa2, gam);
         Particle<FP, LAYOUT>::store(e, i, x, y, z, b_mul(ux, tc.invS), b_mul(uy, tc.invS),
