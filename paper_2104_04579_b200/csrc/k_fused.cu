@@ -270,33 +270,26 @@ struct Particle {
     }
 };
 
-// m-dipole branch grouping.  Each block takes tiles of kMdGroup x kFusedThreads
-// particles; at the start of a launch the particles of a tile whose xi = kR is
-// below xi* (Taylor branch, reading c13) are assigned to the lowest thread slots,
-// the closed-form ones after them, so that at most one warp-round per tile runs
-// both branches (with one particle per thread in storage order, a 0.6-lambda
-// sphere puts a Taylor particle in ~87 % of warps, and a divergent warp executes
-// both bodies).  Scheduling only: every particle's arithmetic is unchanged, so
-// results are bitwise identical to the unpartitioned kernel; particles keep
-// their storage slots (c18).
-#ifndef BORIS_MD_GROUP
-#define BORIS_MD_GROUP 2
-#endif
-constexpr int kMdGroup = BORIS_MD_GROUP;
-
-// Fills s_slot[g * kFusedThreads + t] (g < kMdGroup) with the tile offsets of the
-// particles thread t pushes in round g (-1: none).  Contains two barriers; the
-// caller's loop over tiles must be block-uniform.
+// m-dipole branch ordering.  Before the fused launch, k_md_order writes the particle
+// indices into `order`: those whose xi = kR is below xi* at the launch's first step
+// (Taylor branch, reading c13) from the front, the closed-form ones from the back (each
+// warp reserves its runs with one atomic per branch).  The fused kernel then pushes
+// order[32 r .. 32 r + 31] in warp-round r, so all warp-rounds but the one at the
+// boundary run a single branch (with one particle per thread in storage order, a
+// 0.6-lambda sphere puts a Taylor particle in ~87 % of warps, and a divergent warp
+// executes both bodies), with no barrier and a work unit of one round.  Scheduling
+// only: every particle's arithmetic is unchanged, so results are bitwise identical
+// to the unordered kernel; particles keep their storage slots (c18).
 template <typename FP, int LAYOUT>
-__device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArgs<FP> &fa,
-                                             int64_t base, int *s_slot, int *s_cnt) {
-    constexpr int W = kFusedThreads / 32, Q = kMdGroup * W;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__global__ void __launch_bounds__(256)
+    k_md_order(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa, int *order,
+               unsigned long long *counts) {
+    const int lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
-    unsigned bt[kMdGroup], bc[kMdGroup];
-#pragma unroll
-    for (int g = 0; g < kMdGroup; ++g) {
-        const int64_t i = base + g * kFusedThreads + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < e.n;
+         i0 += stride) {  // warp-uniform
+        const int64_t i = i0 + lane;
         bool taylor = false;
         if (i < e.n) {
             FP x, y, z;
@@ -309,41 +302,24 @@ __device__ __forceinline__ void md_partition(const EnsView &e, const AnalyticArg
                                            i * (sizeof(FP) == 4 ? 36 : 72));
                 x = r[0]; y = r[1]; z = r[2];
             }
-            // the branch test of the first step (k_fused: x = (FP)xa + 0)
-            taylor = md_taylor<FP>(fa, b_norm2(x, y, z));
+            taylor = md_taylor<FP>(fa, b_norm2(x, y, z));  // k_fused's x = (FP)xa + 0
         }
-        bt[g] = __ballot_sync(0xffffffffu, i < e.n && taylor);
-        bc[g] = __ballot_sync(0xffffffffu, i < e.n && !taylor);
+        const unsigned bt = __ballot_sync(0xffffffffu, i < e.n && taylor);
+        const unsigned bc = __ballot_sync(0xffffffffu, i < e.n && !taylor);
+        unsigned long long ft = 0, fc = 0;
         if (lane == 0) {
-            s_cnt[2 * (g * W + warp)] = __popc(bt[g]);
-            s_cnt[2 * (g * W + warp) + 1] = __popc(bc[g]);
+            if (bt) ft = atomicAdd(&counts[0], (unsigned long long)__popc(bt));
+            if (bc) fc = atomicAdd(&counts[1], (unsigned long long)__popc(bc));
+        }
+        ft = __shfl_sync(0xffffffffu, ft, 0);
+        fc = __shfl_sync(0xffffffffu, fc, 0);
+        if (i < e.n) {
+            if (taylor)
+                order[ft + __popc(bt & below)] = (int)i;
+            else
+                order[e.n - 1 - (int64_t)(fc + __popc(bc & below))] = (int)i;
         }
     }
-    __syncthreads();
-    int tot_t = 0, tot_c = 0, pre_t[kMdGroup], pre_c[kMdGroup];
-#pragma unroll
-    for (int g = 0; g < kMdGroup; ++g) pre_t[g] = pre_c[g] = 0;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        const int ct = s_cnt[2 * q], cc = s_cnt[2 * q + 1];
-#pragma unroll
-        for (int g = 0; g < kMdGroup; ++g)
-            if (q < g * W + warp) {
-                pre_t[g] += ct;
-                pre_c[g] += cc;
-            }
-        tot_t += ct;
-        tot_c += cc;
-    }
-#pragma unroll
-    for (int g = 0; g < kMdGroup; ++g) {
-        const int off = g * kFusedThreads + threadIdx.x;
-        const unsigned me = 1u << lane;
-        if (bt[g] & me) s_slot[pre_t[g] + __popc(bt[g] & below)] = off;
-        if (bc[g] & me) s_slot[tot_t + pre_c[g] + __popc(bc[g] & below)] = off;
-        if (off >= tot_t + tot_c) s_slot[off] = -1;
-    }
-    __syncthreads();
 }
 
 }  // namespace
@@ -391,10 +367,53 @@ constexpr int kFlushOf = sizeof(FP) == 4 ? BORIS_FUSED_FLUSH32 : BORIS_FUSED_FLU
 // Launches are split into chunks of kTimeTab steps on the host.
 constexpr int kTimeTab = 1024;
 
+// One Boris step of the single-type m-dipole (kMdFold) in X = k r, u = p/(m c):
+// E = 2 A0 cos(w t) g1 (-Y, X, 0), B = -2 A0 sin(w t) (g2 Z X + f3 z^), xi^2 = |X|^2
+// (eq. 14 in readings c9, c10, c13).  The kick is (q dt/2mc) E = e (-Y, X, 0) with
+// e = tab.y g1, and the rotation vector t = (q dt/2mc) B / gamma_n = a X + b z^ with
+// a = (tab.x / gamma_n) g2 Z, b = (tab.x / gamma_n) f3 (eq. 9-13; E_z = 0 exactly);
+// 1/gamma = rsqrt(1 + |u|^2) (eq. 5 with kappa = 1); the displacement in the window
+// dX += (k c dt / gamma^{n+1/2}) u (eq. 7).  r^n = anchor + d (reading c-fp32r).
+template <typename FP, typename FP2>
+__device__ __forceinline__ void md_fold_step(const FP2 tab, FP xf, FP yf, FP zf, FP &dx, FP &dy,
+                                             FP &dz, FP &ux, FP &uy, FP &uz, FP cr) {
+    const FP x = b_add(xf, dx), y = b_add(yf, dy), z = b_add(zf, dz);
+    FP g1, g2, f3;
+    md_radial_x2<FP>(b_norm2(x, y, z), g1, g2, f3);
+    const FP e = b_mul(tab.y, g1);
+    ux = b_fma(-e, y, ux);
+    uy = b_fma(e, x, uy);
+    const FP tsb = b_mul(tab.x, b_rsqrt(b_fma(ux, ux, b_fma(uy, uy, b_fma(uz, uz, FP(1))))));
+    const FP al = b_mul(tsb, b_mul(g2, z));
+    boris_rotate<FP>(ux, uy, uz, b_mul(al, x), b_mul(al, y), b_fma(al, z, b_mul(tsb, f3)));
+    ux = b_fma(-e, y, ux);
+    uy = b_fma(e, x, uy);
+    const FP ct = b_mul(cr, b_rsqrt(b_fma(ux, ux, b_fma(uy, uy, b_fma(uz, uz, FP(1))))));
+    dx = b_fma(ct, ux, dx);
+    dy = b_fma(ct, uy, dy);
+    dz = b_fma(ct, uz, dz);
+}
+
+// Minimum resident blocks per SM of the m-dipole fused kernels (register cap).  fp32
+// single-type m-dipole, 10^7 x 10^3 steps: 1 (54 registers) 2.77-2.84 ps, 8 (56) 2.70,
+// 10 (40) 2.79-2.88, 12 (40) 2.71 (profiles/r02/exp_mdipole_minb_pair.jsonl).
+#ifndef BORIS_MD_MINB
+#define BORIS_MD_MINB 8
+#endif
+// Particles per thread of the single-type m-dipole kernel (tuning): 2 measured 2.69-2.71
+// ps fp32 (72-80 registers), 8.0 fp64, vs 2.70 / 7.97 with 1.
+#ifndef BORIS_MD_PAIR
+#define BORIS_MD_PAIR 1
+#endif
+constexpr int kMdPair = BORIS_MD_PAIR;
+template <int FIELD>
+constexpr int kFusedMinBlocks = FIELD == FK_MDIPOLE ? BORIS_MD_MINB : 1;
+
 template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER, bool YZ>
-__global__ void __launch_bounds__(kFusedThreads)
+__global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks<FIELD>)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
-            const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_steps, double *partials) {
+            const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_steps, double *partials,
+            const int *__restrict__ order) {
     constexpr int kFlush = kFlushOf<FP>;
     constexpr bool kMerged = kMergedRsqrt<FP, FIELD>;
     __shared__ TypeCoef<FP> s_t[MULTI ? kMaxTypes : 1];
@@ -430,14 +449,7 @@ __global__ void __launch_bounds__(kFusedThreads)
         Particle<FP, LAYOUT>::load(e, i, xa, ya, za, px, py, pz, w, ty);
         if (!MULTI) ty = 0;
         const TypeCoef<FP> tc = MULTI ? s_t[ty] : co.t[0];
-        const FP uin = kMdFold ? fa.mdf_uin : tc.S;
-        FP ux = b_mul(px, uin), uy = b_mul(py, uin), uz = b_mul(pz, uin);
-        if constexpr (kMdFold) {
-            xa *= fa.mdf_k;
-            ya *= fa.mdf_k;
-            za *= fa.mdf_k;
-        }
-        const FP crf = kMdFold ? fa.mdf_cr : tc.cr;
+        FP ux = b_mul(px, tc.S), uy = b_mul(py, tc.S), uz = b_mul(pz, tc.S);
         FP gam = FP(1);
         // uniform / plane wave: E = c e, B = c b with fixed e, b -> per-particle aE e, alpha b
         FP ae[3], ab[3];
@@ -523,29 +535,6 @@ __global__ void __launch_bounds__(kFusedThreads)
                                     b_add((FP)za, dz), Ex, Ey, Ez, Bx, By, Bz);
 #endif
                     inv_g = momentum_update<FP, PUSHER>(ux, uy, uz, Ex, Ey, Ez, Bx, By, Bz, tc, gam);
-                } else if constexpr (kMdFold) {  // eq. 14 (c9, c10, c13), factors folded
-                    // In X = k r: E = 2 A0 cos(w t) g1 (-Y, X, 0), B = -2 A0 sin(w t)
-                    // (g2 Z X + f3 z^), xi^2 = |X|^2.  The kick is (q dt/2mc) E =
-                    // e (-Y, X, 0) with e = tab.y g1, and the rotation vector
-                    // t = (q dt/2mc) B / gamma_n = a X + b z^ with a = (tab.x / gamma_n) g2 Z,
-                    // b = (tab.x / gamma_n) f3 (eq. 9-13; E_z = 0 exactly)
-                    const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
-                    FP g1, g2, f3;
-                    md_radial_x2<FP>(b_norm2(x, y, z), g1, g2, f3);
-                    const FP2 tab = s_tab[s0 + j];
-                    const FP e = b_mul(tab.y, g1);
-                    ux = b_fma(-e, y, ux);
-                    uy = b_fma(e, x, uy);
-                    // 1/gamma_n = rsqrt(1 + |u|^2)  (eq. 5 with kappa = 1)
-                    const FP tsb = b_mul(tab.x, b_rsqrt(b_fma(ux, ux, b_fma(uy, uy,
-                                                                       b_fma(uz, uz, FP(1))))));
-                    const FP al = b_mul(tsb, b_mul(g2, z));
-                    boris_rotate<FP>(ux, uy, uz, b_mul(al, x), b_mul(al, y),
-                                     b_fma(al, z, b_mul(tsb, f3)));
-                    ux = b_fma(-e, y, ux);
-                    uy = b_fma(e, x, uy);
-                    // gamma^{n+1/2} is stored once after the loop
-                    inv_g = b_rsqrt(b_fma(ux, ux, b_fma(uy, uy, b_fma(uz, uz, FP(1)))));
                 } else {  // FK_MDIPOLE, eq. 14 in readings c9, c10, c13
                     FP Ex, Ey, Ez, Bx, By, Bz;
                     const FP x = b_add((FP)xa, dx), y = b_add((FP)ya, dy), z = b_add((FP)za, dz);
@@ -571,7 +560,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                                                             tc, gam);
                 }
                 // a10 (eq. 7): displacement accumulated in the window
-                const FP ct = b_mul(crf, inv_g);
+                const FP ct = b_mul(tc.cr, inv_g);
                 dx = b_fma(ct, ux, dx);
                 dy = b_fma(ct, uy, dy);
                 dz = b_fma(ct, uz, dz);
@@ -590,17 +579,8 @@ __global__ void __launch_bounds__(kFusedThreads)
             ya = __dadd_rn(ya, (double)dy);
             za = __dadd_rn(za, (double)dz);
         }
-        double x = xa, y = ya, z = za;
-        if constexpr (kMdFold) {  // back from X = k r, u = p/(m c); then u = S p as elsewhere
-            x *= fa.mdf_ik;
-            y *= fa.mdf_ik;
-            z *= fa.mdf_ik;
-            ux = b_mul(b_mul(ux, fa.mdf_uout), tc.S);
-            uy = b_mul(b_mul(uy, fa.mdf_uout), tc.S);
-            uz = b_mul(b_mul(uz, fa.mdf_uout), tc.S);
-        }
+        const double x = xa, y = ya, z = za;
         if (n_steps == 0) gam = b_sqrt(b_fma(tc.kappa2, b_norm2(ux, uy, uz), FP(1)));
-        else if (kMdFold) boris_gamma<FP>(ux, uy, uz, tc.kappa2, gam);
         Particle<FP, LAYOUT>::store(e, i, x, y, z, b_mul(ux, tc.invS), b_mul(uy, tc.invS),
                                     b_mul(uz, tc.invS), gam);
         if (DIAG) {
@@ -608,18 +588,88 @@ __global__ void __launch_bounds__(kFusedThreads)
             cnt += 1.0;
         }
     };
-    if constexpr (FIELD == FK_MDIPOLE && kMdGroup > 1) {
-        __shared__ int s_slot[kMdGroup * kFusedThreads];
-        __shared__ int s_cnt[2 * kMdGroup * (kFusedThreads / 32)];
-        const int64_t tile = (int64_t)kMdGroup * kFusedThreads;
-        for (int64_t base = (int64_t)blockIdx.x * tile; base < e.n;
-             base += (int64_t)gridDim.x * tile) {  // block-uniform
-            md_partition<FP, LAYOUT>(e, fa, base, s_slot, s_cnt);
-#pragma unroll 1
-            for (int g = 0; g < kMdGroup; ++g) {
-                const int off = s_slot[g * kFusedThreads + threadIdx.x];
-                if (off >= 0) push_particle(base + off);
+    // kMdFold: kMdPair particles per thread stepped together (kMdPair = 2: two
+    // independent dependency chains per thread, the time-table load and the loop
+    // control shared).  i1 < 0: the second chain repeats particle i0, not stored.
+    auto push_md = [&](int64_t i0, int64_t i1) {
+        constexpr int Q = kMdPair;
+        const TypeCoef<FP> tc = co.t[0];
+        const int64_t ii[2] = {i0, i1 >= 0 ? i1 : i0};
+        double xa[Q], ya[Q], za[Q];
+        FP ux[Q], uy[Q], uz[Q], w[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            FP px, py, pz;
+            int ty;
+            Particle<FP, LAYOUT>::load(e, ii[q], xa[q], ya[q], za[q], px, py, pz, w[q], ty);
+            ux[q] = b_mul(px, fa.mdf_uin);  // u = p/(m c)
+            uy[q] = b_mul(py, fa.mdf_uin);
+            uz[q] = b_mul(pz, fa.mdf_uin);
+            xa[q] *= fa.mdf_k;  // X = k r
+            ya[q] *= fa.mdf_k;
+            za[q] *= fa.mdf_k;
+        }
+        for (int64_t s0 = 0; s0 < n_steps; s0 += kFlush) {
+            FP dx[Q], dy[Q], dz[Q], xf[Q], yf[Q], zf[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                dx[q] = dy[q] = dz[q] = FP(0);
+                xf[q] = (FP)xa[q];
+                yf[q] = (FP)ya[q];
+                zf[q] = (FP)za[q];
             }
+            const int m = (n_steps - s0) < kFlush ? (int)(n_steps - s0) : kFlush;
+            const FP2 *tab = s_tab + s0;
+            for (int j = 0; j < m; ++j) {
+                const FP2 tj = tab[j];
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    md_fold_step<FP>(tj, xf[q], yf[q], zf[q], dx[q], dy[q], dz[q], ux[q], uy[q],
+                                     uz[q], fa.mdf_cr);
+            }
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                xa[q] = __dadd_rn(xa[q], (double)dx[q]);
+                ya[q] = __dadd_rn(ya[q], (double)dy[q]);
+                za[q] = __dadd_rn(za[q], (double)dz[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (q == 1 && i1 < 0) break;
+            // back from X = k r, u = p/(m c); then u = S p as in the other kernels
+            const FP sx = b_mul(b_mul(ux[q], fa.mdf_uout), tc.S);
+            const FP sy = b_mul(b_mul(uy[q], fa.mdf_uout), tc.S);
+            const FP sz = b_mul(b_mul(uz[q], fa.mdf_uout), tc.S);
+            FP gam;
+            if (n_steps == 0)
+                gam = b_sqrt(b_fma(tc.kappa2, b_norm2(sx, sy, sz), FP(1)));
+            else
+                boris_gamma<FP>(sx, sy, sz, tc.kappa2, gam);
+            Particle<FP, LAYOUT>::store(e, ii[q], xa[q] * fa.mdf_ik, ya[q] * fa.mdf_ik,
+                                        za[q] * fa.mdf_ik, b_mul(sx, tc.invS), b_mul(sy, tc.invS),
+                                        b_mul(sz, tc.invS), gam);
+            if (DIAG) {
+                ke += (double)kinetic_energy<FP>(sx, sy, sz, gam, w[q], tc);
+                cnt += 1.0;
+            }
+        }
+    };
+    if constexpr (kMdFold) {  // warp-rounds of 32 kMdPair over the branch order
+        const int64_t nwarp = (int64_t)gridDim.x * (kFusedThreads / 32);
+        constexpr int64_t R = 32 * kMdPair;
+        for (int64_t r = (int64_t)blockIdx.x * (kFusedThreads / 32) + (threadIdx.x >> 5);
+             r * R < e.n; r += nwarp) {
+            const int64_t k = r * R + (threadIdx.x & 31);
+            if (k < e.n)
+                push_md(order[k], (kMdPair == 2 && k + 32 < e.n) ? order[k + 32] : -1);
+        }
+    } else if constexpr (FIELD == FK_MDIPOLE) {  // warp-rounds over the branch order
+        const int64_t nwarp = (int64_t)gridDim.x * (kFusedThreads / 32);
+        for (int64_t r = (int64_t)blockIdx.x * (kFusedThreads / 32) + (threadIdx.x >> 5);
+             r * 32 < e.n; r += nwarp) {
+            const int64_t k = r * 32 + (threadIdx.x & 31);
+            if (k < e.n) push_particle(order[k]);
         }
     } else {
         for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride)
@@ -632,8 +682,8 @@ template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER>
 static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
                                   const Coefs<FP> &co, int64_t n_steps, DiagOut *diag,
                                   int device, cudaStream_t st) {
-    const int64_t per_block = FIELD == FK_MDIPOLE ? (int64_t)kMdGroup * kFusedThreads
-                                                  : (int64_t)kFusedThreads;
+    constexpr bool kPair = FIELD == FK_MDIPOLE && !MULTI && PUSHER == PUSHER_BORIS;  // kMdFold
+    const int64_t per_block = (kPair ? kMdPair : 1) * (int64_t)kFusedThreads;
     const int64_t blocks = (e.n + per_block - 1) / per_block;
     constexpr bool kHasYZ =
         (FIELD == FK_UNIFORM || FIELD == FK_PLANE_WAVE) && PUSHER == PUSHER_BORIS;
@@ -641,10 +691,30 @@ static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
                                         : &k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, false>;
     int64_t grid = fused_grid((const void *)kern, blocks > 0 ? blocks : 1, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
+    int *order = nullptr;
+    if constexpr (FIELD == FK_MDIPOLE) {  // branch order (k_md_order), stream-ordered scratch
+        if (e.n > INT32_MAX) return cudaErrorInvalidValue;
+        cudaError_t err = scratch_alloc((void **)&order, (size_t)e.n * sizeof(int) + 64, st);
+        if (err != cudaSuccess) return err;
+        unsigned long long *counts =
+            (unsigned long long *)((char *)order + (((size_t)e.n * sizeof(int) + 15) / 16) * 16);
+        err = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+        if (err == cudaSuccess) {
+            k_md_order<FP, LAYOUT><<<(unsigned)stream_grid((e.n + 255) / 256, 8, device, 4), 256,
+                                     0, st>>>(e, fa, order, counts);
+            err = cudaGetLastError();
+        }
+        if (err != cudaSuccess) {
+            scratch_free(order, st);
+            return err;
+        }
+    }
     kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, kcoefs<MULTI>(co), n_steps,
-                                                  diag ? diag->partials : nullptr);
+                                                  diag ? diag->partials : nullptr, order);
+    const cudaError_t kerr = cudaGetLastError();
+    if (order) scratch_free(order, st);
     if (diag) diag->written = DIAG ? grid : 0;
-    return cudaGetLastError();
+    return kerr;
 }
 
 template <typename FP, int LAYOUT, int FIELD, int PUSHER>

@@ -119,6 +119,11 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_STREAM_MINB)
 #define BORIS_GRID_MINB 3
 #endif
 #define BORIS_GRID_BOUNDS __launch_bounds__(kStreamThreads, BORIS_GRID_MINB)
+// Preferred shared-memory carveout (percent) of the grid push: -1 leaves the driver's
+// choice (tuning).
+#ifndef BORIS_GRID_CARVEOUT
+#define BORIS_GRID_CARVEOUT -1
+#endif
 template <typename FP, bool MULTI, bool DIAG>
 __global__ void BORIS_GRID_BOUNDS
     k_stream_soa_grid(SoaPtrs s, const __grid_constant__ GridArgs<FP> g,
@@ -211,6 +216,12 @@ static cudaError_t dispatch_soa_grid(const EnsView &e, const GridArgs<FP> &g,
     const int64_t blocks = (n_groups + kStreamThreads - 1) / kStreamThreads;
     int64_t grid = stream_grid(blocks > 0 ? blocks : 1, 2048 / kStreamThreads, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
+    if (BORIS_GRID_CARVEOUT >= 0) {  // L1 / shared split of the SM (the gathers live in L1)
+        static const cudaError_t once = cudaFuncSetAttribute(
+            k_stream_soa_grid<FP, MULTI, DIAG>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            BORIS_GRID_CARVEOUT);
+        if (once != cudaSuccess) return once;
+    }
     k_stream_soa_grid<FP, MULTI, DIAG><<<(unsigned)grid, kStreamThreads, 0, st>>>(
         e.soa, g, kcoefs<MULTI>(co), n_groups, e.n, diag ? diag->partials : nullptr);
     if (diag) diag->written = DIAG ? grid : 0;
