@@ -1138,7 +1138,8 @@ boris_status boris_field_create_grid(int32_t device, boris_precision precision, 
         f->org[d] = origin[d];
         f->h[d] = spacing[d];
     }
-    cudaError_t err = cudaMalloc(&f->nodes, (size_t)ncell * kGridRecord * fp_size(precision));
+    const size_t rec_fp = precision == BORIS_FP32 ? kGridStride<float> : kGridStride<double>;
+    cudaError_t err = cudaMalloc(&f->nodes, (size_t)ncell * rec_fp * fp_size(precision));
     if (err != cudaSuccess) {
         delete f;
         return cuda_fail(err, "cudaMalloc(grid nodes)");

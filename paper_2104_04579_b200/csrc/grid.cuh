@@ -15,7 +15,7 @@ constexpr int kGridRecord = 12;  // FP per x-pair record: [E B](i) [E B](i+1)
 
 template <typename FP>
 struct GridArgs {
-    const FP *nodes;  // x-pair records (12 FP), record (i,j,k) at (k*ny + j)*nx + i
+    const FP *nodes;  // x-pair records (12 FP, kGridStride apart), record (i,j,k) at (k*ny + j)*nx + i
     FP org[3];        // origin
     FP inv_h[3];      // 1 / spacing
     FP nf[3];         // n as FP
@@ -59,24 +59,53 @@ __device__ __forceinline__ uint32_t grid_cell(const GridArgs<FP> &g, FP x, FP y,
     return ((uint32_t)k0 * (uint32_t)g.n[1] + (uint32_t)j0) * (uint32_t)g.n[0] + (uint32_t)i0;
 }
 
+// FP between consecutive records in the nodes buffer.  BORIS_GRID_LDG256 (tuning): a
+// record is read with 256-bit loads (sm_100 LDG.256) -- fp32 pads the 48 B record to
+// 64 B so every record starts on a 32 B boundary (one 256-bit + one 128-bit load),
+// fp64's 96 B records are three 256-bit loads.  Measured (10^7, 64^3): single-step
+// push sorted fp32 11.56-11.73 vs 11.52-11.55 ps with 16 B loads, fp64 26.1 vs 22.4, PIC
+// cycle 25.3 both (profiles/r02/exp_grid_ldg256.jsonl): off (3 / 6 16 B loads).
+#ifndef BORIS_GRID_LDG256
+#define BORIS_GRID_LDG256 0
+#endif
+template <typename FP>
+constexpr int kGridStride = (sizeof(FP) == 4 && BORIS_GRID_LDG256) ? 16 : kGridRecord;
+
 // The two x-nodes (i0, i0+1 mod nx) of a cell row: one x-pair record, 12 FP,
-// e[0..5] = [E B](i0), e[6..11] = [E B](i0+1): three 128-bit loads in fp32, six
-// in fp64.  (The gathers are bound by L1 requests, 16 per particle with one
-// 8-FP record per node; 12 with pair records.)
+// e[0..5] = [E B](i0), e[6..11] = [E B](i0+1): 12 loads per particle with 16 B loads
+// (16 with one 8-FP record per node).
 __device__ __forceinline__ void load_pair(const float *nodes, uint32_t rec, float (&e)[12]) {
-    const float4 *p = reinterpret_cast<const float4 *>(nodes) + 3 * (size_t)rec;
-    const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+    const float *p = nodes + kGridStride<float> * (size_t)rec;
+#if BORIS_GRID_LDG256
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(e[0]), "=f"(e[1]), "=f"(e[2]), "=f"(e[3]), "=f"(e[4]), "=f"(e[5]), "=f"(e[6]),
+          "=f"(e[7])
+        : "l"(p));
+    const float4 c = __ldg(reinterpret_cast<const float4 *>(p + 8));
+    e[8] = c.x; e[9] = c.y; e[10] = c.z; e[11] = c.w;
+#else
+    const float4 *q = reinterpret_cast<const float4 *>(p);
+    const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
     e[0] = a.x; e[1] = a.y; e[2] = a.z; e[3] = a.w; e[4] = b.x; e[5] = b.y;
     e[6] = b.z; e[7] = b.w; e[8] = c.x; e[9] = c.y; e[10] = c.z; e[11] = c.w;
+#endif
 }
 __device__ __forceinline__ void load_pair(const double *nodes, uint32_t rec, double (&e)[12]) {
-    const double2 *p = reinterpret_cast<const double2 *>(nodes) + 6 * (size_t)rec;
+    const double *p = nodes + kGridStride<double> * (size_t)rec;
+#if BORIS_GRID_LDG256
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(e[4 * k]), "=d"(e[4 * k + 1]), "=d"(e[4 * k + 2]), "=d"(e[4 * k + 3])
+            : "l"(p + 4 * k));
+#else
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-        const double2 v = __ldg(p + k);
+        const double2 v = __ldg(reinterpret_cast<const double2 *>(p) + k);
         e[2 * k] = v.x;
         e[2 * k + 1] = v.y;
     }
+#endif
 }
 
 // E, B at (x, y, z): sum over the 8 nodes of the cell of wx wy wz F_node.

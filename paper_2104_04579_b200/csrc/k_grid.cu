@@ -18,8 +18,9 @@ namespace boris {
 
 // ---------------------------------------------------------------------------
 // Node packing into x-pair records: record i holds node i and its +x neighbour
-// (periodic), 12 FP = [E B](i) [E B](i+1): the CIC gather loads a cell's two
-// x-nodes with 3 (fp32) / 6 (fp64) 128-bit loads, 12 per particle instead of 16.
+// (periodic), 12 FP = [E B](i) [E B](i+1) (grid.cuh kGridStride apart): the CIC
+// gather loads a cell's two x-nodes with 3 (fp32) / 6 (fp64) 128-bit loads, 12 per
+// particle instead of 16 with one record per node.
 // ---------------------------------------------------------------------------
 template <typename FP>
 __global__ void k_grid_pack(int64_t ncell, int nx, const FP *Ex, const FP *Ey, const FP *Ez,
@@ -28,11 +29,13 @@ __global__ void k_grid_pack(int64_t ncell, int nx, const FP *Ex, const FP *Ey, c
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell; i += stride) {
         const int64_t ix = i % nx;
         const int64_t i1 = i - ix + (ix + 1 == nx ? 0 : ix + 1);
-        FP *r = nodes + kGridRecord * i;
+        FP *r = nodes + kGridStride<FP> * i;
         r[0] = Ex[i];  r[1] = Ey[i];  r[2] = Ez[i];
         r[3] = Bx[i];  r[4] = By[i];  r[5] = Bz[i];
         r[6] = Ex[i1]; r[7] = Ey[i1]; r[8] = Ez[i1];
         r[9] = Bx[i1]; r[10] = By[i1]; r[11] = Bz[i1];
+#pragma unroll
+        for (int k = kGridRecord; k < kGridStride<FP>; ++k) r[k] = FP(0);  // padding
     }
 }
 
