@@ -113,11 +113,16 @@ const char *boris_last_error(void);
  *   BORIS_OPT_HOST_CHUNK (particles, default 4194304): chunk size of the
  *     host-resident (BORIS_MEMORY_HOST) push pipeline; must be >= 1024, used
  *     rounded down to a multiple of 8.
+ *   BORIS_OPT_MD_ORDER (0 or 1, default 1): 1 lets a fused m-dipole push
+ *     schedule the particles by radial branch (Taylor ones first, reading c13;
+ *     a scratch index list of 4 n bytes); 0 pushes them in storage order.
+ *     Scheduling only: results are bitwise identical; for tests.
  * A new value applies to pushes issued after the call.  Errors: INVALID_ARG
  * (unknown option, value out of range, NULL out-pointer).
  */
 #define BORIS_OPT_FUSED_GENERIC 1
 #define BORIS_OPT_HOST_CHUNK 2
+#define BORIS_OPT_MD_ORDER 3
 boris_status boris_set_option(int32_t option, int64_t value);
 boris_status boris_get_option(int32_t option, int64_t *value);
 

@@ -44,6 +44,7 @@ BORIS_PUSH_PUSHER_VAY = 0x10
 BORIS_PUSH_PUSHER_HIGUERA_CARY = 0x20
 BORIS_PUSH_PUSHER_MASK = 0x30
 BORIS_OPT_FUSED_GENERIC = 1
+BORIS_OPT_MD_ORDER = 3
 BORIS_OPT_HOST_CHUNK = 2
 BORIS_AOS_RECORD_BYTES = {BORIS_FP32: 36, BORIS_FP64: 72}
 BORIS_AOS_FIELD_BYTES = {BORIS_FP32: 24, BORIS_FP64: 48}

@@ -17,6 +17,7 @@
 // Process-wide options (boris_set_option); the library reads no environment.
 static std::atomic<int64_t> g_opt_fused_generic{0};
 static std::atomic<int64_t> g_opt_host_chunk{(int64_t)4 << 20};
+static std::atomic<int64_t> g_opt_md_order{1};
 
 using namespace boris;
 
@@ -335,6 +336,7 @@ AnalyticArgs<FP> make_analytic(const boris_field *f, double t0, double dt) {
         a.mA02 = (FP)(-2.0 * f->A0);
         a.w0t0 = f->omega0 * t0;
         a.w0dt = f->omega0 * dt;
+        a.md_order = (int)g_opt_md_order.load(std::memory_order_relaxed);
     } else if (f->kind == FK_GRID) {
         a.grid = make_grid_args<FP>(f);
     }
@@ -629,6 +631,11 @@ boris_status boris_set_option(int32_t option, int64_t value) {
                         (long long)value);
         g_opt_host_chunk.store(value);
         return BORIS_OK;
+    case BORIS_OPT_MD_ORDER:
+        if (value != 0 && value != 1)
+            return fail(BORIS_E_INVALID_ARG, "BORIS_OPT_MD_ORDER must be 0 or 1");
+        g_opt_md_order.store(value);
+        return BORIS_OK;
     default:
         return fail(BORIS_E_INVALID_ARG, "unknown option %d", option);
     }
@@ -639,6 +646,7 @@ boris_status boris_get_option(int32_t option, int64_t *value) {
     switch (option) {
     case BORIS_OPT_FUSED_GENERIC: *value = g_opt_fused_generic.load(); return BORIS_OK;
     case BORIS_OPT_HOST_CHUNK: *value = g_opt_host_chunk.load(); return BORIS_OK;
+    case BORIS_OPT_MD_ORDER: *value = g_opt_md_order.load(); return BORIS_OK;
     default: return fail(BORIS_E_INVALID_ARG, "unknown option %d", option);
     }
 }

@@ -49,6 +49,7 @@ struct AnalyticArgs {
     FP A0k2;         // 2 A0 k
     FP mA02;         // -2 A0
     double w0t0, w0dt;
+    int md_order;  // schedule by radial branch (k_md_order; BORIS_OPT_MD_ORDER)
     // single-type Boris m-dipole (k_fused kMdFold; push_view fills these): the step runs
     // in the scaled variables X = k r, u = p/(m c), so that xi^2 = |X|^2 and
     // gamma^2 = 1 + |u|^2 (no k^2, kappa^2 factors in the loop)

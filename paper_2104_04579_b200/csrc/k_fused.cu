@@ -662,14 +662,15 @@ __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks<FIELD>)
              r * R < e.n; r += nwarp) {
             const int64_t k = r * R + (threadIdx.x & 31);
             if (k < e.n)
-                push_md(order[k], (kMdPair == 2 && k + 32 < e.n) ? order[k + 32] : -1);
+                push_md(order ? order[k] : k,
+                        (kMdPair == 2 && k + 32 < e.n) ? (order ? order[k + 32] : k + 32) : -1);
         }
     } else if constexpr (FIELD == FK_MDIPOLE) {  // warp-rounds over the branch order
         const int64_t nwarp = (int64_t)gridDim.x * (kFusedThreads / 32);
         for (int64_t r = (int64_t)blockIdx.x * (kFusedThreads / 32) + (threadIdx.x >> 5);
              r * 32 < e.n; r += nwarp) {
             const int64_t k = r * 32 + (threadIdx.x & 31);
-            if (k < e.n) push_particle(order[k]);
+            if (k < e.n) push_particle(order ? order[k] : k);
         }
     } else {
         for (int64_t i = (int64_t)blockIdx.x * kFusedThreads + threadIdx.x; i < e.n; i += stride)
@@ -691,22 +692,27 @@ static cudaError_t dispatch_fused(const EnsView &e, const AnalyticArgs<FP> &fa,
                                         : &k_fused<FP, LAYOUT, FIELD, MULTI, DIAG, PUSHER, false>;
     int64_t grid = fused_grid((const void *)kern, blocks > 0 ? blocks : 1, device);
     if (DIAG && grid > diag->cap) grid = diag->cap;
-    int *order = nullptr;
+    int *order = nullptr;  // nullptr: storage order
     if constexpr (FIELD == FK_MDIPOLE) {  // branch order (k_md_order), stream-ordered scratch
-        if (e.n > INT32_MAX) return cudaErrorInvalidValue;
-        cudaError_t err = scratch_alloc((void **)&order, (size_t)e.n * sizeof(int) + 64, st);
-        if (err != cudaSuccess) return err;
-        unsigned long long *counts =
-            (unsigned long long *)((char *)order + (((size_t)e.n * sizeof(int) + 15) / 16) * 16);
-        err = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
-        if (err == cudaSuccess) {
-            k_md_order<FP, LAYOUT><<<(unsigned)stream_grid((e.n + 255) / 256, 8, device, 4), 256,
-                                     0, st>>>(e, fa, order, counts);
-            err = cudaGetLastError();
-        }
-        if (err != cudaSuccess) {
-            scratch_free(order, st);
-            return err;
+        // (scheduling only: above 2^31 particles, or without scratch memory, the kernel
+        // pushes in storage order)
+        if (fa.md_order && e.n <= INT32_MAX &&
+            scratch_alloc((void **)&order, (size_t)e.n * sizeof(int) + 64, st) == cudaSuccess) {
+            unsigned long long *counts = (unsigned long long *)((char *)order +
+                                                                (((size_t)e.n * 4 + 15) / 16) * 16);
+            cudaError_t err = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+            if (err == cudaSuccess) {
+                k_md_order<FP, LAYOUT><<<(unsigned)stream_grid((e.n + 255) / 256, 8, device, 4),
+                                         256, 0, st>>>(e, fa, order, counts);
+                err = cudaGetLastError();
+            }
+            if (err != cudaSuccess) {
+                scratch_free(order, st);
+                return err;
+            }
+        } else {
+            (void)cudaGetLastError();  // a failed pool allocation is not sticky
+            order = nullptr;
         }
     }
     kern<<<(unsigned)grid, kFusedThreads, 0, st>>>(e, fa, kcoefs<MULTI>(co), n_steps,

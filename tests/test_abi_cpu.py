@@ -125,13 +125,16 @@ def test_options_are_abi_calls_not_environment(lb):
     assert lb.boris_get_option(lb.BORIS_OPT_FUSED_GENERIC) == 0
     chunk0 = lb.boris_get_option(lb.BORIS_OPT_HOST_CHUNK)
     assert chunk0 == 4 << 20
+    assert lb.boris_get_option(lb.BORIS_OPT_MD_ORDER) == 1
     try:
+        lb.boris_set_option(lb.BORIS_OPT_MD_ORDER, 0)
+        assert lb.boris_get_option(lb.BORIS_OPT_MD_ORDER) == 0
         lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 1)
         assert lb.boris_get_option(lb.BORIS_OPT_FUSED_GENERIC) == 1
         lb.boris_set_option(lb.BORIS_OPT_HOST_CHUNK, 4096)
         assert lb.boris_get_option(lb.BORIS_OPT_HOST_CHUNK) == 4096
         for opt, bad in ((lb.BORIS_OPT_FUSED_GENERIC, 2), (lb.BORIS_OPT_HOST_CHUNK, 1023),
-                         (99, 0)):
+                         (lb.BORIS_OPT_MD_ORDER, -1), (99, 0)):
             with pytest.raises(lb.BorisError) as ei:
                 lb.boris_set_option(opt, bad)
             assert ei.value.status == lb.BORIS_E_INVALID_ARG
@@ -140,6 +143,7 @@ def test_options_are_abi_calls_not_environment(lb):
     finally:
         lb.boris_set_option(lb.BORIS_OPT_FUSED_GENERIC, 0)
         lb.boris_set_option(lb.BORIS_OPT_HOST_CHUNK, chunk0)
+        lb.boris_set_option(lb.BORIS_OPT_MD_ORDER, 1)
     # (the static CUDA runtime linked into libboris.so reads CUDA_* variables itself;
     # libboris' own sources never call getenv)
     import glob

@@ -434,6 +434,44 @@ def test_mdipole_branch_grouping_is_scheduling_only(precision, layout):
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+@pytest.mark.parametrize("multi", [False, True])
+def test_mdipole_branch_order_is_scheduling_only(precision, layout, multi):
+    """The fused m-dipole push schedules particles by radial branch (k_md_order,
+    Taylor ones first); BORIS_OPT_MD_ORDER = 0 pushes them in storage order.  Both
+    must give bitwise identical states (single type: the scaled-variable kernel;
+    multi-type: the generic one), n not a multiple of 32 or 64."""
+    w = mdipole_workload()
+    if multi:
+        w.types = [synth.ELECTRON, synth.POSITRON]
+        w.type_mix = "random"
+    n = 5 * 1024 + 29
+    d = rounded(w.generate(0, n), precision)
+    cls = SoaEnsemble if layout == "soa" else AosEnsemble
+    field = gpu_field(w)
+    states = []
+    try:
+        for order in (1, 0):
+            lb.boris_set_option(lb.BORIS_OPT_MD_ORDER, order)
+            e = cls(n, PREC[precision], w.types, w.light_velocity)
+            e.fill(d)
+            e.wrap()
+            diag = torch.zeros(2, dtype=torch.float64, device="cuda")
+            lb.boris_push_diag(e.handle, field, w.dt, 60, diag.data_ptr())
+            torch.cuda.synchronize()
+            states.append((e.state(), diag.clone()))
+            e.close()
+    finally:
+        lb.boris_set_option(lb.BORIS_OPT_MD_ORDER, 1)
+    (a, da), (b, db) = states
+    for k in ("x", "y", "z", "px", "py", "pz", "gamma"):
+        assert torch.equal(a[k], b[k]), k
+    assert da[1].item() == db[1].item() == n
+    assert abs(da[0].item() - db[0].item()) <= 1e-12 * abs(db[0].item())  # block sums reorder
+    lb.boris_field_destroy(field)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_mdipole_parity(precision):
     w = mdipole_workload()
     worst = run_parity(w, "soa", precision, N_SMALL, checks=(1, 2, 10, 100))
