@@ -44,6 +44,16 @@ template <typename FP>
 constexpr bool kTransposedMerge = sizeof(FP) == 4 && BORIS_DEP_MERGE_T;
 template <typename FP>
 constexpr bool kTransposedMergePD = sizeof(FP) == 4 && BORIS_PD_MERGE_T;
+// Lane-run sums in moment form (DepositRun; tuning): 1 accumulates q w v times the
+// monomials 1, fx, fy, fx fy, fz, fx fz, fy fz, fx fy fz of the particle's in-cell
+// offsets (4 products instead of 15 operations for the node weights) and converts the
+// run sums to the 8 node sums at each flush / run end (across lanes by shuffles in
+// the transposed merge).  Measured slower (10^7 sorted, 64^3: deposition 10.85 vs
+// 10.22 ps, fused PIC cycle 28.6 vs 25.3; profiles/r02/exp_deposit_moments.jsonl):
+// 0 accumulates q w v times the 8 node weights.
+#ifndef BORIS_DEP_MOMENTS
+#define BORIS_DEP_MOMENTS 0
+#endif
 // lanes per group whose 24 sums are added as one partial sum when no run ends in it
 #ifndef BORIS_MERGE_GROUP
 #define BORIS_MERGE_GROUP 4
@@ -107,7 +117,7 @@ __device__ __forceinline__ void red_cell(const DepOut<FP> &o, uint32_t nb, const
 
 template <typename FP>
 struct DepositRun {
-    FP acc[8][3];
+    FP acc[8][3];  // BORIS_DEP_MOMENTS: moment k = (kz*2 + ky)*2 + kx sums; else node q sums
     uint32_t nb;  // J4 base node of the open cell (kNoNode: none)
     FP fl[3];     // the open cell's unwrapped floor((r - org)/h)
 
@@ -118,11 +128,27 @@ struct DepositRun {
         fl[0] = fl[1] = fl[2] = FP(0);
     }
 
+    // Moment sums -> node sums (in place): per axis, node (offset 0) = M(1) - M(f) and
+    // node (offset 1) = M(f), since the CIC weights are (1 - f, f) (reading c-dep);
+    // node q = (c*2 + b)*2 + a as corner().
+    __device__ __forceinline__ void to_nodes() {
+#if BORIS_DEP_MOMENTS
+#pragma unroll
+        for (int sb = 1; sb < 8; sb <<= 1)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (!(k & sb))
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) acc[k][d] = b_add(acc[k][d], -acc[k | sb][d]);
+#endif
+    }
+
     // Atomics for the open cell (if any), then zero the sums (LAST: the run ends
     // here and is reset before any reuse, so the sums are left as they are).
     template <bool LAST = false>
     __device__ __forceinline__ void flush(const DepOut<FP> &o) {
         if (nb == kNoNode) return;
+        to_nodes();
         red_cell(o, nb, acc);
         if constexpr (!LAST) {
 #pragma unroll
@@ -130,60 +156,82 @@ struct DepositRun {
         }
     }
 
-    // One particle (state after the push: r^{n+1}, p^{n+1/2}, weight w).
-    __device__ __forceinline__ void add(const GridArgs<FP> &g, const DepOut<FP> &o,
-                                        const DepCoef<FP> &t, FP half_dt, FP x, FP y, FP z,
-                                        FP px, FP py, FP pz, FP w) {
+    // One particle's CIC data: unwrapped cell l, in-cell offsets f and their
+    // products (moments) or the 8 node weights, and q w v / cell volume.
+    struct Part {
+        FP l[3];
+        FP m[8];  // moments: 1 (unused), fx, fy, fx fy, fz, fx fz, fy fz, fx fy fz; or weights
+        FP qv[3];
+    };
+
+    // State after the push: r^{n+1}, p^{n+1/2}, weight w (reading c-dep: r^{n+1/2} =
+    // r^{n+1} - (dt/2) v^{n+1/2}).
+    static __device__ __forceinline__ void prepare(const GridArgs<FP> &g, const DepCoef<FP> &t,
+                                                   FP half_dt, FP x, FP y, FP z, FP px, FP py,
+                                                   FP pz, FP w, Part &p) {
         const FP ux = b_mul(px, t.S), uy = b_mul(py, t.S), uz = b_mul(pz, t.S);
-        // v = p/(gamma m) = u/(S m gamma)
         const FP vf = b_mul(t.inv_Sm, b_rsqrt(b_fma(t.kappa2, b_norm2(ux, uy, uz), FP(1))));
         const FP vx = b_mul(ux, vf), vy = b_mul(uy, vf), vz = b_mul(uz, vf);
-        FP f[3], l[3];
-        l[0] = axis_floor(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], f[0]);
-        l[1] = axis_floor(b_fma(-half_dt, vy, y), g.org[1], g.inv_h[1], f[1]);
-        l[2] = axis_floor(b_fma(-half_dt, vz, z), g.org[2], g.inv_h[2], f[2]);
-        // same unwrapped cell -> same nodes; a periodic image of the open cell only
-        // costs an extra flush
-        if (nb == kNoNode || l[0] != fl[0] || l[1] != fl[1] || l[2] != fl[2]) {
-            flush(o);
-            fl[0] = l[0]; fl[1] = l[1]; fl[2] = l[2];
-            nb = base_node(g, o, l);
-        }
+        FP f[3];
+        p.l[0] = axis_floor(b_fma(-half_dt, vx, x), g.org[0], g.inv_h[0], f[0]);
+        p.l[1] = axis_floor(b_fma(-half_dt, vy, y), g.org[1], g.inv_h[1], f[1]);
+        p.l[2] = axis_floor(b_fma(-half_dt, vz, z), g.org[2], g.inv_h[2], f[2]);
+        const FP qw = b_mul(t.q_vol, w);
+        p.qv[0] = b_mul(qw, vx);
+        p.qv[1] = b_mul(qw, vy);
+        p.qv[2] = b_mul(qw, vz);
+#if BORIS_DEP_MOMENTS
+        p.m[0] = FP(1);
+        p.m[1] = f[0];
+        p.m[2] = f[1];
+        p.m[3] = b_mul(f[0], f[1]);
+        p.m[4] = f[2];
+        p.m[5] = b_mul(f[0], f[2]);
+        p.m[6] = b_mul(f[1], f[2]);
+        p.m[7] = b_mul(p.m[3], f[2]);
+#else
         const FP wx[2] = {b_add(FP(1), -f[0]), f[0]};
         const FP wy[2] = {b_add(FP(1), -f[1]), f[1]};
         const FP wz[2] = {b_add(FP(1), -f[2]), f[2]};
-        const FP qw = b_mul(t.q_vol, w);
 #pragma unroll
         for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
-                const FP wyz = b_mul(qw, b_mul(wy[b], wz[c]));
+                const FP wyz = b_mul(wy[b], wz[c]);
 #pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                    const int q = (c * 2 + b) * 2 + a;
-                    const FP sw = b_mul(wx[a], wyz);
-                    acc[q][0] = b_fma(sw, vx, acc[q][0]);
-                    acc[q][1] = b_fma(sw, vy, acc[q][1]);
-                    acc[q][2] = b_fma(sw, vz, acc[q][2]);
-                }
+                for (int a = 0; a < 2; ++a) p.m[(c * 2 + b) * 2 + a] = b_mul(wx[a], wyz);
             }
+#endif
     }
 
-    // One particle prepared by WarpRun<FP>::prepare (unwrapped cell, node weights,
-    // q w v / volume): the cell test and the 24 FMA only, so a caller can prepare
-    // several particles first (independent chains) and accumulate them after.
-    template <typename Part>
+    // One particle (state after the push).
+    __device__ __forceinline__ void add(const GridArgs<FP> &g, const DepOut<FP> &o,
+                                        const DepCoef<FP> &t, FP half_dt, FP x, FP y, FP z,
+                                        FP px, FP py, FP pz, FP w) {
+        Part p;
+        prepare(g, t, half_dt, x, y, z, px, py, pz, w, p);
+        add_part(g, o, p);
+    }
+
+    // One prepared particle: the cell test and the 24 accumulations only, so a caller
+    // can prepare several particles first (independent chains) and accumulate them after.
     __device__ __forceinline__ void add_part(const GridArgs<FP> &g, const DepOut<FP> &o,
                                              const Part &p) {
+        // same unwrapped cell -> same nodes; a periodic image of the open cell only
+        // costs an extra flush
         if (nb == kNoNode || p.l[0] != fl[0] || p.l[1] != fl[1] || p.l[2] != fl[2]) {
             flush(o);
             fl[0] = p.l[0]; fl[1] = p.l[1]; fl[2] = p.l[2];
             nb = base_node(g, o, p.l);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+        for (int d = 0; d < 3; ++d)
+            acc[0][d] = BORIS_DEP_MOMENTS ? b_add(acc[0][d], p.qv[d])
+                                          : b_fma(p.m[0], p.qv[d], acc[0][d]);
 #pragma unroll
-            for (int d = 0; d < 3; ++d) acc[q][d] = b_fma(p.sw[q], p.qv[d], acc[q][d]);
+        for (int q = 1; q < 8; ++q)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) acc[q][d] = b_fma(p.m[q], p.qv[d], acc[q][d]);
     }
 
     // End of a warp tile (all 32 lanes): lanes holding the same open cell in
@@ -281,6 +329,15 @@ struct DepositRun {
                     const int l = g0 + gv * VW + k;
                     run = b_add(run, v[gv][k]);
                     if (tails & (1u << l)) {  // warp-uniform
+#if BORIS_DEP_MOMENTS
+                        // lane 3k + d holds moment k of component d: to node sums
+                        // (to_nodes across the lanes)
+#pragma unroll
+                        for (int sb = 1; sb < 8; sb <<= 1) {
+                            const FP other = __shfl_sync(full, run, 3 * (q ^ sb) + d);
+                            if (!(q & sb)) run = b_add(run, -other);
+                        }
+#endif
                         const FP ry = __shfl_down_sync(full, run, 1);
                         const FP rz = __shfl_down_sync(full, run, 2);
                         if (lane < 24 && d == 0)

@@ -751,10 +751,10 @@ __global__ void __launch_bounds__(kDepWarps * 32, BORIS_DEP_DIRECT_MINB)
             // then the cell tests and accumulations
 #pragma unroll
             for (int h = 0; h < kDepK; h += 4) {
-                WarpRun<float>::Part pp[4];
+                DepositRun<float>::Part pp[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    WarpRun<float>::prepare(g, dc.t[multi ? rty[h + j] : 0], dc.half_dt,
+                    DepositRun<float>::prepare(g, dc.t[multi ? rty[h + j] : 0], dc.half_dt,
                                             rv[0][h + j], rv[1][h + j], rv[2][h + j],
                                             rv[3][h + j], rv[4][h + j], rv[5][h + j],
                                             rv[6][h + j], pp[j]);

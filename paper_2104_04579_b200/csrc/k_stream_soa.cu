@@ -346,10 +346,10 @@ __global__ void __launch_bounds__(kStreamThreads, BORIS_PD_MINB)
             // stored p after the stores beats carrying the push's u and 1/gamma)
 #if BORIS_PD_PREP
             {   // the V particles' weights first (independent chains), then accumulate
-                typename WarpRun<FP>::Part pp[V];
+                typename DepositRun<FP>::Part pp[V];
 #pragma unroll
                 for (int j = 0; j < V; ++j)
-                    WarpRun<FP>::prepare(g, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j],
+                    DepositRun<FP>::prepare(g, MULTI ? s_d[ty[j]] : dc.t[0], dc.half_dt, x.v[j],
                                          y.v[j], z.v[j], px.v[j], py.v[j], pz.v[j], w.v[j], pp[j]);
 #pragma unroll
                 for (int j = 0; j < V; ++j) run.add_part(g, o, pp[j]);
