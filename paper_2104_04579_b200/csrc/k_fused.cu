@@ -394,9 +394,13 @@ __device__ __forceinline__ void md_fold_step(const FP2 tab, FP xf, FP yf, FP zf,
     dz = b_fma(ct, uz, dz);
 }
 
-// Minimum resident blocks per SM of the m-dipole fused kernels (register cap).  fp32
-// single-type m-dipole, 10^7 x 10^3 steps: 1 (54 registers) 2.77-2.84 ps, 8 (56) 2.70,
-// 10 (40) 2.79-2.88, 12 (40) 2.71 (profiles/r02/exp_mdipole_minb_pair.jsonl).
+// Minimum resident blocks per SM in the fused kernels' launch bounds (0: none given).
+// m-dipole: a register cap; fp32 single-type m-dipole, 10^7 x 10^3 steps: none (54
+// registers) 2.77-2.84 ps, 8 (56) 2.70, 10 (40) 2.79-2.88, 12 (40) 2.71
+// (profiles/r02/exp_mdipole_minb_pair.jsonl).  fp32 grid: an explicit 1 lets ptxas take
+// 116 instead of 105 registers (100 fused steps, 10^7 sorted: 5.69 vs 5.87 ps); every
+// other field keeps none -- an explicit 1 took C4 from 48 to 80 registers (1.18 ->
+// 1.24 ps) and the fp64 grid kernel from 158 to 184 (10.9 -> 13.0 ps).
 #ifndef BORIS_MD_MINB
 #define BORIS_MD_MINB 8
 #endif
@@ -406,11 +410,13 @@ __device__ __forceinline__ void md_fold_step(const FP2 tab, FP xf, FP yf, FP zf,
 #define BORIS_MD_PAIR 1
 #endif
 constexpr int kMdPair = BORIS_MD_PAIR;
-template <int FIELD>
-constexpr int kFusedMinBlocks = FIELD == FK_MDIPOLE ? BORIS_MD_MINB : 1;
+template <typename FP, int FIELD>
+constexpr int kFusedMinBlocks = FIELD == FK_MDIPOLE                    ? BORIS_MD_MINB
+                                : (FIELD == FK_GRID && sizeof(FP) == 4) ? 1
+                                                                        : 0;
 
 template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER, bool YZ>
-__global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks<FIELD>)
+__global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks<FP, FIELD>)
     k_fused(EnsView e, const __grid_constant__ AnalyticArgs<FP> fa,
             const __grid_constant__ KCoefs<FP, MULTI> co, int64_t n_steps, double *partials,
             const int *__restrict__ order) {
