@@ -400,7 +400,10 @@ __device__ __forceinline__ void md_fold_step(const FP2 tab, FP xf, FP yf, FP zf,
 // (profiles/r02/exp_mdipole_minb_pair.jsonl).  fp32 grid: an explicit 1 lets ptxas take
 // 116 instead of 105 registers (100 fused steps, 10^7 sorted: 5.69 vs 5.87 ps); every
 // other field keeps none -- an explicit 1 took C4 from 48 to 80 registers (1.18 ->
-// 1.24 ps) and the fp64 grid kernel from 158 to 184 (10.9 -> 13.0 ps).
+// 1.24 ps) and the fp64 grid kernel from 158 to 184 (10.9 -> 13.0 ps).  Sweep of the
+// tuning knobs below (profiles/r02/exp_fused_minblocks_sweep.jsonl): fp64 m-dipole 5 / 6
+// / 10 blocks 7.94 / 7.94 / 8.05 vs 7.86 ps with 8; uniform 1 / 10 C3 2.35 / 2.40 vs
+// 2.33; plane wave 1 / 12 C4 1.24 / 1.20 vs 1.18.
 #ifndef BORIS_MD_MINB
 #define BORIS_MD_MINB 8
 #endif
@@ -410,10 +413,22 @@ __device__ __forceinline__ void md_fold_step(const FP2 tab, FP xf, FP yf, FP zf,
 #define BORIS_MD_PAIR 1
 #endif
 constexpr int kMdPair = BORIS_MD_PAIR;
+#ifndef BORIS_MD_MINB64
+#define BORIS_MD_MINB64 BORIS_MD_MINB
+#endif
+#ifndef BORIS_UNIFORM_MINB
+#define BORIS_UNIFORM_MINB 0
+#endif
+#ifndef BORIS_PLANE_MINB
+#define BORIS_PLANE_MINB 0
+#endif
 template <typename FP, int FIELD>
-constexpr int kFusedMinBlocks = FIELD == FK_MDIPOLE                    ? BORIS_MD_MINB
-                                : (FIELD == FK_GRID && sizeof(FP) == 4) ? 1
-                                                                        : 0;
+constexpr int kFusedMinBlocks =
+    FIELD == FK_MDIPOLE                     ? (sizeof(FP) == 4 ? BORIS_MD_MINB : BORIS_MD_MINB64)
+    : (FIELD == FK_GRID && sizeof(FP) == 4) ? 1
+    : FIELD == FK_UNIFORM                   ? BORIS_UNIFORM_MINB
+    : FIELD == FK_PLANE_WAVE                ? BORIS_PLANE_MINB
+                                            : 0;
 
 template <typename FP, int LAYOUT, int FIELD, bool MULTI, bool DIAG, int PUSHER, bool YZ>
 __global__ void __launch_bounds__(kFusedThreads, kFusedMinBlocks<FP, FIELD>)
