@@ -355,6 +355,13 @@ __global__ void k_scan_add(uint32_t *data, int64_t len, const uint32_t *chunk_of
 #ifndef BORIS_SCAN_LOOKBACK
 #define BORIS_SCAN_LOOKBACK 1
 #endif
+// look-back chunks: 16 values per thread (a 10^7-particle histogram of 2.5 M entries
+// is 153 chunks, one wave)
+#ifndef BORIS_SCAN_LB_ITEMS
+#define BORIS_SCAN_LB_ITEMS 16
+#endif
+constexpr int kLbItems = BORIS_SCAN_LB_ITEMS;
+constexpr int kLbChunk = kScanThreads * kLbItems;
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_lookback(uint32_t *data, int64_t len, unsigned long long *status, unsigned *ticket) {
     __shared__ uint32_t s_w[kScanThreads / 32];
@@ -363,13 +370,21 @@ __global__ void __launch_bounds__(kScanThreads)
     if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t chunk = s_chunk;
-    const int64_t c0 = (int64_t)chunk * kScanChunk + (int64_t)threadIdx.x * kScanItems;
-    uint32_t v[kScanItems], sum = 0;
+    const int64_t c0 = (int64_t)chunk * kLbChunk + (int64_t)threadIdx.x * kLbItems;
+    uint32_t v[kLbItems], sum = 0;
+    const bool full = c0 + kLbItems <= len && ((uintptr_t)data & 15u) == 0;  // uint4 access
+    if (full) {
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        v[k] = (c0 + k < len) ? data[c0 + k] : 0u;
-        sum += v[k];
+        for (int k = 0; k < kLbItems / 4; ++k) {
+            const uint4 q4 = reinterpret_cast<const uint4 *>(data + c0)[k];
+            v[4 * k] = q4.x; v[4 * k + 1] = q4.y; v[4 * k + 2] = q4.z; v[4 * k + 3] = q4.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kLbItems; ++k) v[k] = (c0 + k < len) ? data[c0 + k] : 0u;
     }
+#pragma unroll
+    for (int k = 0; k < kLbItems; ++k) sum += v[k];
     uint32_t inc = sum;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -418,9 +433,20 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
     uint32_t run = s_excl + inc - sum + (warp > 0 ? s_w[warp - 1] : 0u);  // exclusive prefix
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        if (c0 + k < len) data[c0 + k] = run;
-        run += v[k];
+    for (int k = 0; k < kLbItems; ++k) {
+        const uint32_t x = v[k];
+        v[k] = run;
+        run += x;
+    }
+    if (full) {
+#pragma unroll
+        for (int k = 0; k < kLbItems / 4; ++k)
+            reinterpret_cast<uint4 *>(data + c0)[k] =
+                make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kLbItems; ++k)
+            if (c0 + k < len) data[c0 + k] = v[k];
     }
 }
 
@@ -432,13 +458,14 @@ static cudaError_t exclusive_scan(uint32_t *data, int64_t len, cudaStream_t st) 
     }
     cudaError_t err;
     if (BORIS_SCAN_LOOKBACK) {
+        const int64_t lchunks = (len + kLbChunk - 1) / kLbChunk;
         unsigned long long *status = nullptr;
-        const size_t bytes = (size_t)(chunks + 1) * sizeof(unsigned long long);
+        const size_t bytes = (size_t)(lchunks + 1) * sizeof(unsigned long long);
         if ((err = scratch_alloc((void **)&status, bytes, st)) != cudaSuccess) return err;
         err = cudaMemsetAsync(status, 0, bytes, st);
         if (err == cudaSuccess) {
-            k_scan_lookback<<<(unsigned)chunks, kScanThreads, 0, st>>>(
-                data, len, status, (unsigned *)(status + chunks));
+            k_scan_lookback<<<(unsigned)lchunks, kScanThreads, 0, st>>>(
+                data, len, status, (unsigned *)(status + lchunks));
             err = cudaGetLastError();
         }
         scratch_free(status, st);
