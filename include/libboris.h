@@ -338,8 +338,9 @@ boris_status boris_push_deposit(boris_ensemble *ens, const boris_field *grid, do
  * device and residency must match, else MISMATCH).  The values are those the
  * fused push uses at (r_i, t), to rounding: the m-dipole is evaluated with the
  * fused step's radial functions and branch (reading c13), but the single-type
- * Boris fused push folds the type's coefficients into the field's scalar
- * factors instead of forming E and B.  Device ensembles only.  Asynchronous.
+ * Boris fused push works in the scaled variables k r and p/(m c) and folds the
+ * type's coefficients into the field's scalar factors instead of forming E and
+ * B (a few roundings apart).  Device ensembles only.  Asynchronous.
  */
 boris_status boris_field_evaluate(const boris_field *analytic, const boris_ensemble *ens,
                                   double t, const boris_field *out, void *stream);
