@@ -1101,12 +1101,14 @@ def test_grid_fused_push_with_frequent_cell_crossings():
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("layout", ["soa", "aos"])
-def test_sort_by_cell_is_a_stable_permutation(precision, layout):
+@pytest.mark.parametrize("n", [3 * 2048 + 333, 300_000 + 17])
+def test_sort_by_cell_is_a_stable_permutation(precision, layout, n):
+    """n = 300017: 147 radix tiles x 512 digits = 75264 histogram entries, scanned by
+    the single-pass look-back kernel in 5 chunks with a ragged last one."""
     h, params, gE, gB = grid_setup(precision, nx=9, ny=7, nz=5)
     w = synth.config("C2")
     w.types = [synth.ELECTRON, synth.POSITRON, synth.PROTON]
     w.type_mix = "random"
-    n = 3 * 2048 + 333
     d = rounded(w.generate(0, n), precision)
     d["weight"] = torch.arange(n, dtype=torch.float64)      # particle id (exact)
     cls = SoaEnsemble if layout == "soa" else AosEnsemble
