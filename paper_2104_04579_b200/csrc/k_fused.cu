@@ -88,17 +88,12 @@ struct MdBranch<float> {  // reading c13: fp32 xi* = 1.5, 7 terms
     static constexpr int terms = 7;
 };
 
-// R = |r| for the m-dipole: fp32 R2 rsqrt(R2) with the MUFU rsqrt (<= 2 ulp, like
-// every other fp32 square root of the push; R = 0 at the origin) unless
-// BORIS_PRECISE_MATH; fp64 correctly rounded.
-__device__ __forceinline__ float md_radius(float r2) {
 #ifdef BORIS_PRECISE_MATH
-    return __fsqrt_rn(r2);
-#else
-    return r2 > 0.f ? b_mul(r2, b_rsqrt(r2)) : 0.f;
-#endif
-}
+// R = |r| for the m-dipole with BORIS_PRECISE_MATH (correctly rounded square roots; the
+// default math works with xi^2 and never forms R, md_radial_x2 below).
+__device__ __forceinline__ float md_radius(float r2) { return __fsqrt_rn(r2); }
 __device__ __forceinline__ double md_radius(double r2) { return __dsqrt_rn(r2); }
+#endif
 
 // Closed-form branch of the radial functions (eq. 15, reading c11) from s = sin xi,
 // c = cos xi and i = 1/xi, factored so that each product is formed once:
