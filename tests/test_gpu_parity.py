@@ -436,7 +436,8 @@ def test_mdipole_branch_grouping_is_scheduling_only(precision, layout):
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("layout", ["soa", "aos"])
 @pytest.mark.parametrize("multi", [False, True])
-def test_mdipole_branch_order_is_scheduling_only(precision, layout, multi):
+@pytest.mark.parametrize("n", [5 * 1024 + 29, 1, 33])
+def test_mdipole_branch_order_is_scheduling_only(precision, layout, multi, n):
     """The fused m-dipole push schedules particles by radial branch (k_md_order,
     Taylor ones first); BORIS_OPT_MD_ORDER = 0 pushes them in storage order.  Both
     must give bitwise identical states (single type: the scaled-variable kernel;
@@ -445,7 +446,6 @@ def test_mdipole_branch_order_is_scheduling_only(precision, layout, multi):
     if multi:
         w.types = [synth.ELECTRON, synth.POSITRON]
         w.type_mix = "random"
-    n = 5 * 1024 + 29
     d = rounded(w.generate(0, n), precision)
     cls = SoaEnsemble if layout == "soa" else AosEnsemble
     field = gpu_field(w)
