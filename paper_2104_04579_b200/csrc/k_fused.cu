@@ -162,7 +162,7 @@ __device__ __forceinline__ void md_radial_x2(FP x2, FP &g1, FP &g2, FP &f3) {
 }
 
 // The radial functions from r^2 = |r|^2 (field evaluation, the multi-type and
-// alternative-pusher fused steps, the branch grouping): xi^2 = k^2 r^2 as above;
+// alternative-pusher fused steps, the branch ordering k_md_order): xi^2 = k^2 r^2 as above;
 // BORIS_PRECISE_MATH uses R = sqrt(r^2), xi = k R with correctly rounded square root
 // and reciprocal.
 template <typename FP>

@@ -403,9 +403,10 @@ def mdipole_workload():
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 @pytest.mark.parametrize("layout", ["soa", "aos"])
 def test_mdipole_branch_grouping_is_scheduling_only(precision, layout):
-    """The fused m-dipole kernel regroups each tile's particles by radial branch
-    (k_fused.cu md_partition).  Pushing slices that start at offsets unrelated to
-    the tile size groups different particles together; results must not change."""
+    """The fused m-dipole kernel schedules particles by radial branch (k_fused.cu
+    k_md_order: Taylor ones first, in warp-rounds over the order list).  Pushing
+    slices of the ensemble groups different particles into the same warp-rounds;
+    results must not change."""
     w = mdipole_workload()
     n = 3 * 4096 + 37
     d = rounded(w.generate(0, n), precision)
